@@ -1,0 +1,317 @@
+"""Benchmark of the stencil-sweep hot path (BASELINE.json metric, config 2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one pass of the hot path over one batch: config 2 (all ten
+4th-order outputs of a 256^3 fp64 box with 2 ghost layers, the
+configuration the north-star gate is quoted on).  Prints ONE JSON line on
+rank 0.  `value` is whole-job grid-point updates/s with inputs resident in
+HBM (CUDA events on the launching stream, max over ranks); `e2e` repeats
+the metric through the public API with the input copied from pinned host
+memory and all ten outputs copied back inside the timed region.
+
+Multi-GPU (torchrun): every rank sweeps its own 256^3 box — independent
+units, no data-path collective — so scaling is weak; the only
+communication is a barrier and the max-over-ranks time.
+
+`--impl reference` times the reference's algorithm on the host cores: the
+CPU oracle port (oracle/, numpy expression trees in the reference's
+_update_rows style driven by its static thread split), rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "stencil grid-pt updates/s (config 2: 4th-order 10-output sweep, 256^3 fp64)"
+UNIT = "Gpts/s"
+WORKLOAD = {"workload": "config2_d4_all_256^3", "interior": [256, 256, 256], "ghost": 2, "outputs": 10,
+            "dtype": "f64", "h": "1/256", "field": "sin(2pi x)sin(2pi y)sin(2pi z) + 1e-3 U[-1,1]",
+            "l2": "no flush: per-step working set 1.48 GB >> 126 MB L2"}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except ValueError:
+            pass
+    return {}
+
+
+def ncu_traffic() -> float | None:
+    """dram bytes (read+write) per d4_all launch from the committed ncu summary."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        return float(d["d4_all"]["dram_bytes_per_launch"])
+    except (ValueError, KeyError, TypeError):
+        return None
+
+
+class ClockSampler:
+    """Samples SM clock and clock-event reasons through NVML while running."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting",
+               0x10: "sync_boost"}
+
+    def __init__(self, index: int, period: float = 0.01):
+        self.index, self.period = index, period
+        self.mhz: list[int] = []
+        self.reasons: set[str] = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.mhz.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+        return False
+
+    def summary(self) -> dict:
+        return {"sm_mhz": statistics.median(self.mhz) if self.mhz else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.mhz)}
+
+
+class CpuOracle:
+    """The oracle port over z-slabs of config 2 with all host threads."""
+
+    def __init__(self, planes: int = 8):
+        import oracle
+        from oracle.stencils import host_threads
+        from paper_1308_1343_b200 import inputs
+        self.oracle = oracle
+        self.n, self.g, self.planes = 256, 2, planes
+        self.u = inputs.c2_field(self.n, self.g)
+        self.k = inputs.D4Constants.for_spacing(1.0 / self.n)
+        self.threads = host_threads()
+        self.outs = [np.empty((planes, self.n, self.n)) for _ in range(10)]
+        self.z = 0
+
+    def slab(self) -> float:
+        """One slab of `planes` z-planes (all ten outputs); returns seconds."""
+        n, g, P = self.n, self.g, self.planes
+        z0 = self.z
+        self.z = (self.z + P) % (n - P + 1)
+
+        def work(a, b):
+            ds = self.oracle.stencils.derivs9(self.u, g, (0, n, 0, n, z0 + a, z0 + b), self.k)
+            lap = (ds[3] + ds[4]) + ds[5]
+            for o, v in zip(self.outs, ds + [lap]):
+                o[a:b] = v
+        t0 = time.perf_counter()
+        self.oracle.run_static(work, 0, P, self.threads)
+        return time.perf_counter() - t0
+
+    def sample(self, seconds: float) -> dict:
+        done, el = 0, 0.0
+        while el < seconds:
+            el += self.slab()
+            done += self.planes
+        pts = done * self.n * self.n
+        return {"value": pts / el / 1e9, "unit": UNIT, "cores": self.threads, "kind": "port",
+                "sample": f"{done} z-planes of 256x256 (= {pts} updates, {done // self.planes} slabs of "
+                          f"{self.planes} planes) of config 2, oracle numpy expression trees over "
+                          f"{self.threads} threads, {el:.2f} s"}
+
+
+def run_reference(args) -> None:
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cpu = CpuOracle()
+    for _ in range(args.warmup):
+        cpu.slab()
+    secs = [cpu.slab() for _ in range(args.steps)]
+    pts = cpu.planes * cpu.n * cpu.n
+    v = statistics.median([pts / s / 1e9 for s in secs])
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 256 ** 3 / (v * 1e9) * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded host generator, BASELINE.json config 2 shapes)",
+           "config": dict(WORKLOAD, parallelism=f"host threads x{cpu.threads}"),
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu.threads, "kind": "port",
+                            "sample": f"each step: one slab of {cpu.planes} z-planes of 256x256 of config 2 "
+                                      f"({pts} updates), oracle numpy expression trees, {cpu.threads} threads; "
+                                      f"value = median over {args.steps} steps; ms_per_step extrapolated to 256^3"},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def run_ours(args) -> None:
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1308_1343_b200 import _build
+    from paper_1308_1343_b200.configs import C2FourthOrder
+    from paper_1308_1343_b200.tuner import LaunchParams
+
+    if rank == 0 or not _build.LIB.exists():
+        _build.build()
+    if dist:
+        dist.barrier()
+
+    prob = C2FourthOrder().setup()
+    params = LaunchParams(*args.params) if args.params else prob.kernel.default_params
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        prob.run(params)
+    barrier()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with ClockSampler(local) as clk:
+        ev[0].record(stream)
+        for i in range(args.steps):
+            prob.run(params)
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    ms_total = ev[0].elapsed_time(ev[-1])
+    ms_total = max_over_ranks(ms_total)
+    ms_step = ms_total / args.steps
+    updates = prob.updates * world
+    value = updates / (ms_step * 1e-3) / 1e9
+
+    # e2e through the public API: pinned host input -> device -> 10 outputs -> pinned host
+    n = prob.n
+    h_in = torch.from_numpy(prob.host_u).pin_memory()
+    h_out = [torch.empty((n, n, n), dtype=torch.float64).pin_memory() for _ in range(10)]
+    out_ptrs = [t.data_ptr() for t in h_out]
+    e2e_steps = max(3, min(args.steps, args.e2e_steps))
+    for _ in range(2):
+        prob.e2e_step(h_in.data_ptr(), out_ptrs, params)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk_e2e:
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            prob.e2e_step(h_in.data_ptr(), out_ptrs, params)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
+    e2e_value = updates / (e2e_ms * 1e-3) / 1e9
+    # results really came back: spot-check the host copy of Lap4 against the device
+    ok = torch.equal(h_out[9][:2].cuda(), prob.outs[9].interior()[:2])
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    peaks = measured_peaks()
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    kernel_ms = statistics.mean(per)
+    achieved = prob.canonical_bytes / (kernel_ms * 1e-3) / 1e9
+    traffic = ncu_traffic()
+    cpu = None if args.no_cpu or world > 1 else CpuOracle().sample(args.ref_seconds)
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded host generator, BASELINE.json config 2 shapes)",
+        "config": dict(WORKLOAD, parallelism=f"box-per-rank x{world}",
+                       launch={"tile_x": params.tile_x, "tile_y": params.tile_y, "z_chunk": params.z_chunk}),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks else "fallback",
+                     "algorithmic_bytes_per_launch": prob.canonical_bytes, "kernel_ms_mean": kernel_ms,
+                     "kernel_ms_median": statistics.median(per), "kernel": "d4_kernel<ALL10> (sb_d4_all)"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": prob.h2d_bytes,
+                "d2h_bytes_per_step": prob.d2h_bytes, "ms_per_step": e2e_ms, "steps": e2e_steps,
+                "results_checked": bool(ok)},
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+        "clocks_e2e": clk_e2e.summary(),
+    }
+    print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--params", type=int, nargs=3, default=None, metavar=("TILE_X", "TILE_Y", "Z_CHUNK"))
+    ap.add_argument("--e2e-steps", dest="e2e_steps", type=int, default=10)
+    ap.add_argument("--ref-seconds", dest="ref_seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", dest="no_cpu", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,178 @@
+/*
+ * stencil_b200.h — C ABI of libstencil_b200.so, the B200 (sm_100a) hot path
+ * behind the reference's loop-iterator / stencil-kernel plugin interface.
+ *
+ * The reference (package `stencilrt`, pure Python) has no native code; its
+ * plugin boundary is `Kernel = Callable[[IndexSpace], None]`
+ * (pkg/src/stencilrt/traverse.py:159) called by `execute_plan`
+ * (traverse.py:162-209) / `run_loop` (traverse.py:220-232) /
+ * `run_static` (traverse.py:235-260), with the arithmetic in
+ * `_update_rows` (stencil.py:31-39).  Each entry point below replaces one
+ * such kernel body for a whole index space (or a whole bboxset level) in a
+ * single launch.  The Python host layer binds these through ctypes
+ * (paper_1308_1343_b200/_lib.py); INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - Grids are fp64, x contiguous (the reference's numpy (z,y,x) C-order,
+ *    stencil.py:9-10).  `sb_array.origin` points at interior point (0,0,0);
+ *    element (x,y,z) is origin[x + y*sy + z*sz] for -ghost <= x,y,z <
+ *    n+ghost.  Every row additionally owns `xpad` readable elements before
+ *    x = 0 so rows start 128-byte aligned (TMA base).
+ *  - Index spaces are half-open [lo, hi), innermost dimension first, in
+ *    interior coordinates (traverse.py:31-56 uses the same ordering).
+ *  - Arithmetic is IEEE fp64, one rounding per + - *, association exactly as
+ *    the reference's numpy expression trees (no FMA contraction; the library
+ *    is built with -fmad=false and uses __d*_rn intrinsics).  This is the
+ *    reference's unfused-FMA contract, vlanes.py:33 / vlanes.py:243-249.
+ *  - All launches are asynchronous on the caller's stream (a cudaStream_t
+ *    passed as void*; NULL = legacy default stream).  No entry point
+ *    allocates or frees caller memory.
+ *  - Return codes: SB_OK, SB_USAGE (contract violation, maps to the
+ *    reference's UsageError, lattice.py:22), SB_RESOURCE (ResourceError,
+ *    lattice.py:26), SB_CUDA (CUDA failure).  sb_last_error() returns a
+ *    thread-local message for the last failing call.  No C++ exception
+ *    crosses this boundary.
+ */
+#ifndef STENCIL_B200_H
+#define STENCIL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SB_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define SB_API __attribute__((visibility("default")))
+#else
+#define SB_API
+#endif
+
+#define SB_OK 0
+#define SB_USAGE 1
+#define SB_RESOURCE 2
+#define SB_CUDA 3
+
+#define SB_MAX_BOXES 8     /* boxes per batched launch (sb_lap4_boxes) */
+#define SB_N_D4_OUT 10     /* Dx Dy Dz Dxx Dyy Dzz Dxy Dxz Dyz Lap4 */
+#define SB_N_VARS 24       /* config-5 grid functions */
+#define SB_N_TERMS 64      /* config-5 terms per output polynomial */
+
+/* One fp64 grid in device memory (the device-resident form of the numpy
+ * arrays the reference's kernels close over, stencil.py:42-46). */
+typedef struct sb_array {
+    double *origin;   /* interior (0,0,0); 16-byte aligned */
+    int64_t sy;       /* row pitch in elements (even) */
+    int64_t sz;       /* plane pitch in elements (even) */
+    int32_t nx, ny, nz; /* interior extents */
+    int32_t ghost;    /* ghost width on every face */
+    int32_t xpad;     /* readable elements before x = 0 in a row (>= ghost, even) */
+} sb_array;
+
+/* Half-open index space, innermost first (traverse.py:31-56). */
+typedef struct sb_space {
+    int32_t lo[3];
+    int32_t hi[3];
+} sb_space;
+
+/* One point of the GPU tuning space (the device counterpart of the
+ * reference's ExecParams, tuner.py:99-111): CTA tile in x and y, and the
+ * number of z planes one CTA streams.  tile_x is a multiple of 32. */
+typedef struct sb_launch {
+    int32_t tile_x;
+    int32_t tile_y;
+    int32_t z_chunk;
+    int32_t flags;    /* reserved, 0 */
+} sb_launch;
+
+/* 4th-order constants: k1 = 1/(12h), k2 = 1/(12h^2), k11 = 1/(144h^2). */
+typedef struct sb_d4_constants {
+    double k1, k2, k11;
+} sb_d4_constants;
+
+/* One box of a refinement level: its source grid (ghost >= 2), the output
+ * grid and the index space to update (interior coordinates of the box). */
+typedef struct sb_box_job {
+    sb_array dst;
+    sb_array src;
+    sb_space space;
+} sb_box_job;
+
+/* Classical RK4 state for the scalar wave equation (phi, pi). */
+typedef struct sb_rk4_fields {
+    sb_array phi_s;   /* stencil input of this stage (ghost >= 2, filled) */
+    sb_array pi_s;    /* pi of this stage (unused by stage 1) */
+    sb_array phi0, pi0;   /* state at the start of the step */
+    sb_array acc_phi, acc_pi; /* running k1 + 2k2 + 2k3 (in place) */
+    sb_array phi_out, pi_out; /* next stage (or new state at stage 4) */
+} sb_rk4_fields;
+
+typedef struct sb_rk4_constants {
+    sb_d4_constants lap;
+    double half_dt, dt, dt6;
+} sb_rk4_constants;
+
+/* Config-5 polynomial table, row-major [output][term]. */
+typedef struct sb_poly {
+    const double *coef;   /* SB_N_VARS * SB_N_TERMS */
+    const int32_t *p;     /* input index 10*var + slot, 0..239 */
+    const int32_t *q;
+} sb_poly;
+
+typedef struct sb_device_info {
+    int32_t device, sm_count, cc_major, cc_minor;
+    int64_t l2_bytes, smem_optin_bytes, global_mem_bytes;
+} sb_device_info;
+
+SB_API int sb_abi_version(void);
+SB_API const char *sb_last_error(void);
+SB_API int sb_init(int device);
+SB_API int sb_get_device_info(sb_device_info *info);
+
+/* K0 — vlanes.forward_difference (vlanes.py:342-349) when kind == 0:
+ * dst[i] = src[i+1] - src[i], 0 <= i < n-1;  vlanes.centered_difference
+ * (vlanes.py:352-360) when kind == 1: dst[i] = 0.5*(src[i+1]-src[i-1]),
+ * 1 <= i < n-1.  Lanes outside the range never store (iterate_masked,
+ * vlanes.py:322-337). */
+SB_API int sb_diff1d(int32_t kind, double *dst, const double *src, int32_t n, void *stream);
+
+/* K1 — 7-point update (stencil.py:31-39, _update_rows):
+ * dst = c0*b + c1*(((xm+xp) + (ym+yp)) + (zm+zp)) over `space`. */
+SB_API int sb_lap7(sb_array dst, sb_array src, sb_space space, double c0, double c1,
+            sb_launch p, void *stream);
+
+/* K2 — all ten 4th-order outputs of one box (config 2).  out[i] follows
+ * SB_N_D4_OUT order.  src ghost >= 2. */
+SB_API int sb_d4_all(const sb_array *out, sb_array src, sb_space space,
+              sb_d4_constants k, sb_launch p, void *stream);
+
+/* K3 — 4th-order Laplacian over up to SB_MAX_BOXES boxes of a level in one
+ * launch (config 4); the device box table replaces execute_plan's block
+ * queue (traverse.py:162-209). */
+SB_API int sb_lap4_boxes(const sb_box_job *jobs, int32_t njobs, sb_d4_constants k,
+                  sb_launch p, void *stream);
+
+/* K4 — periodic refill of the ghost shell of `a` (every ghost point becomes
+ * the interior point at its periodic image). */
+SB_API int sb_ghost_periodic(sb_array a, void *stream);
+
+/* K5 — one classical RK4 stage (1..4) of d/dt(phi, pi) = (pi, Lap4 phi). */
+SB_API int sb_rk4_stage(int32_t stage, const sb_rk4_fields *f, sb_space space,
+                 sb_rk4_constants c, sb_launch p, void *stream);
+
+/* K6 — config-5 fused right-hand side: 24 inputs (ghost >= 2) -> 24 outputs. */
+SB_API int sb_rhs24(const sb_array *in, const sb_array *out, sb_space space,
+             sb_d4_constants k, sb_poly poly, sb_launch p, void *stream);
+
+/* Host <-> device transfer of a whole ghosted grid (with_ghosts = 1) or of
+ * its interior (0).  `host` is dense (z,y,x), x contiguous. */
+SB_API int sb_copy_h2d(sb_array dst, const double *host, int32_t with_ghosts, void *stream);
+SB_API int sb_copy_d2h(double *host, sb_array src, int32_t with_ghosts, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STENCIL_B200_H */

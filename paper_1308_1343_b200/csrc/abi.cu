@@ -1,0 +1,295 @@
+// abi.cu — extern "C" entry points of libstencil_b200.so (include/stencil_b200.h).
+//
+// Validation mirrors the reference's contract checks: inverted index spaces
+// and bad shapes are usage errors (traverse.py:36-42 raises UsageError), as
+// are geometry violations of the device layout (alignment, ghost width).
+// Resource limits (shared memory, boxes per launch) are ResourceError-class.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace sb {
+
+namespace {
+thread_local std::string t_last_error;
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+std::once_flag g_encode_once;
+
+void resolve_encode() {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+        g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Geometry contract of an sb_array; `need_ghost` is the stencil radius read.
+int check_array(const sb_array &a, int need_ghost, const char *name) {
+    char buf[256];
+    if (!a.origin) {
+        snprintf(buf, sizeof buf, "%s: null origin", name);
+        return fail(SB_USAGE, buf);
+    }
+    if (!aligned16(a.origin) || (a.sy & 1) || (a.sz & 1) || (a.xpad & 1)) {
+        snprintf(buf, sizeof buf, "%s: origin must be 16-byte aligned and sy, sz, xpad even", name);
+        return fail(SB_USAGE, buf);
+    }
+    if (a.nx < 0 || a.ny < 0 || a.nz < 0 || a.ghost < 0 || a.xpad < a.ghost) {
+        snprintf(buf, sizeof buf, "%s: negative extent or xpad < ghost", name);
+        return fail(SB_USAGE, buf);
+    }
+    if (a.sy < (int64_t)a.xpad + a.nx + a.ghost || a.sz < a.sy * (int64_t)(a.ny + 2 * a.ghost)) {
+        snprintf(buf, sizeof buf, "%s: strides too small for extents", name);
+        return fail(SB_USAGE, buf);
+    }
+    if (a.ghost < need_ghost) {
+        snprintf(buf, sizeof buf, "%s: ghost width %d < stencil radius %d", name, a.ghost, need_ghost);
+        return fail(SB_USAGE, buf);
+    }
+    return SB_OK;
+}
+
+int check_space(const sb_space &s, const sb_array &a, const char *name) {
+    char buf[256];
+    const int n[3] = {a.nx, a.ny, a.nz};
+    for (int d = 0; d < 3; ++d) {
+        if (s.hi[d] < s.lo[d]) {
+            snprintf(buf, sizeof buf, "%s: index space with inverted bounds in dim %d", name, d);
+            return fail(SB_USAGE, buf);
+        }
+        if (s.hi[d] > s.lo[d] && (s.lo[d] < 0 || s.hi[d] > n[d])) {
+            snprintf(buf, sizeof buf, "%s: index space [%d,%d) outside interior 0..%d in dim %d", name, s.lo[d],
+                     s.hi[d], n[d], d);
+            return fail(SB_USAGE, buf);
+        }
+    }
+    return SB_OK;
+}
+
+cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+int fail(int code, const std::string &msg) {
+    t_last_error = msg;
+    return code;
+}
+
+int check_cuda(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return SB_OK;
+    t_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+    return SB_CUDA;
+}
+
+int make_tmap(CUtensorMap *m, const sb_array &a, int bx, int by, int bz) {
+    std::call_once(g_encode_once, resolve_encode);
+    if (!g_encode) return fail(SB_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    double *base = a.origin - a.xpad - (int64_t)a.ghost * a.sy - (int64_t)a.ghost * a.sz;
+    if (!aligned16(base)) return fail(SB_USAGE, "TMA base (row start of the first ghost row) not 16-byte aligned");
+    cuuint64_t dims[3] = {(cuuint64_t)a.sy, (cuuint64_t)(a.ny + 2 * a.ghost), (cuuint64_t)(a.nz + 2 * a.ghost)};
+    cuuint64_t strides[2] = {(cuuint64_t)a.sy * 8, (cuuint64_t)a.sz * 8};
+    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d) for box %dx%dx%d", (int)r, bx, by, bz);
+        return fail(SB_CUDA, buf);
+    }
+    return SB_OK;
+}
+
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" {
+
+int sb_abi_version(void) { return SB_ABI_VERSION; }
+
+const char *sb_last_error(void) { return t_last_error.c_str(); }
+
+int sb_init(int device) {
+    int rc = check_cuda(cudaSetDevice(device), "cudaSetDevice");
+    if (rc) return rc;
+    return check_cuda(cudaFree(nullptr), "context init");
+}
+
+int sb_get_device_info(sb_device_info *info) {
+    if (!info) return fail(SB_USAGE, "null info");
+    int dev = 0;
+    int rc = check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    if (rc) return rc;
+    cudaDeviceProp p;
+    rc = check_cuda(cudaGetDeviceProperties(&p, dev), "cudaGetDeviceProperties");
+    if (rc) return rc;
+    info->device = dev;
+    info->sm_count = p.multiProcessorCount;
+    info->cc_major = p.major;
+    info->cc_minor = p.minor;
+    info->l2_bytes = p.l2CacheSize;
+    info->smem_optin_bytes = (int64_t)p.sharedMemPerBlockOptin;
+    info->global_mem_bytes = (int64_t)p.totalGlobalMem;
+    return SB_OK;
+}
+
+int sb_diff1d(int32_t kind, double *dst, const double *src, int32_t n, void *stream) {
+    if (kind != 0 && kind != 1) return fail(SB_USAGE, "diff1d: kind must be 0 (forward) or 1 (centered)");
+    if (n < 0) return fail(SB_USAGE, "diff1d: negative length");
+    if (n > 0 && (!dst || !src)) return fail(SB_USAGE, "diff1d: null pointer");
+    return launch_diff1d(kind, dst, src, n, as_stream(stream));
+}
+
+int sb_lap7(sb_array dst, sb_array src, sb_space space, double c0, double c1, sb_launch p, void *stream) {
+    int rc;
+    if ((rc = check_array(src, 1, "lap7 src")) || (rc = check_array(dst, 0, "lap7 dst"))) return rc;
+    if ((rc = check_space(space, src, "lap7")) || (rc = check_space(space, dst, "lap7 dst"))) return rc;
+    return launch_lap7(dst, src, space, c0, c1, p, as_stream(stream));
+}
+
+int sb_d4_all(const sb_array *out, sb_array src, sb_space space, sb_d4_constants k, sb_launch p, void *stream) {
+    int rc;
+    if (!out) return fail(SB_USAGE, "d4_all: null output table");
+    if ((rc = check_array(src, 2, "d4_all src")) || (rc = check_space(space, src, "d4_all"))) return rc;
+    D4Job job;
+    memset(&job, 0, sizeof(job));
+    job.src = src;
+    job.space = space;
+    for (int i = 0; i < SB_N_D4_OUT; ++i) {
+        if ((rc = check_array(out[i], 0, "d4_all out")) || (rc = check_space(space, out[i], "d4_all out")))
+            return rc;
+        job.g[i] = out[i];
+    }
+    return launch_d4(D4_ALL10, &job, 1, k, 0.0, 0.0, p, as_stream(stream));
+}
+
+int sb_lap4_boxes(const sb_box_job *jobs, int32_t njobs, sb_d4_constants k, sb_launch p, void *stream) {
+    if (njobs == 0) return SB_OK;
+    if (!jobs || njobs < 0) return fail(SB_USAGE, "lap4_boxes: bad job table");
+    if (njobs > SB_MAX_BOXES) return fail(SB_RESOURCE, "lap4_boxes: more than SB_MAX_BOXES boxes in one launch");
+    D4Job dj[SB_MAX_BOXES];
+    memset(dj, 0, sizeof(dj));
+    int rc;
+    for (int j = 0; j < njobs; ++j) {
+        if ((rc = check_array(jobs[j].src, 2, "lap4 src")) || (rc = check_array(jobs[j].dst, 0, "lap4 dst")))
+            return rc;
+        if ((rc = check_space(jobs[j].space, jobs[j].src, "lap4")) ||
+            (rc = check_space(jobs[j].space, jobs[j].dst, "lap4 dst")))
+            return rc;
+        dj[j].src = jobs[j].src;
+        dj[j].space = jobs[j].space;
+        dj[j].g[0] = jobs[j].dst;
+    }
+    return launch_d4(D4_LAP4, dj, njobs, k, 0.0, 0.0, p, as_stream(stream));
+}
+
+int sb_ghost_periodic(sb_array a, void *stream) {
+    int rc = check_array(a, 0, "ghost_periodic");
+    if (rc) return rc;
+    return launch_ghost_periodic(a, as_stream(stream));
+}
+
+int sb_rk4_stage(int32_t stage, const sb_rk4_fields *f, sb_space space, sb_rk4_constants c, sb_launch p,
+                 void *stream) {
+    if (!f) return fail(SB_USAGE, "rk4_stage: null fields");
+    if (stage < 1 || stage > 4) return fail(SB_USAGE, "rk4_stage: stage must be 1..4");
+    int rc;
+    if ((rc = check_array(f->phi_s, 2, "rk4 phi_s")) || (rc = check_space(space, f->phi_s, "rk4"))) return rc;
+    const sb_array *pw[] = {&f->pi_s, &f->phi0, &f->pi0, &f->acc_phi, &f->acc_pi, &f->phi_out, &f->pi_out};
+    for (const sb_array *a : pw) {
+        if (stage == 1 && (a == &f->pi_s || a == &f->phi0)) continue;
+        if ((rc = check_array(*a, 0, "rk4 field")) || (rc = check_space(space, *a, "rk4 field"))) return rc;
+    }
+    D4Job job;
+    memset(&job, 0, sizeof(job));
+    job.src = f->phi_s;
+    job.space = space;
+    job.g[0] = f->phi_out;
+    job.g[1] = f->pi_out;
+    job.g[2] = f->acc_phi;
+    job.g[3] = f->acc_pi;
+    int mode;
+    double ca;
+    if (stage == 1) {
+        job.g[4] = f->pi0;
+        mode = D4_RK1;
+        ca = c.half_dt;
+    } else {
+        job.g[4] = f->pi_s;
+        job.g[5] = f->phi0;
+        job.g[6] = f->pi0;
+        job.g[7] = f->acc_phi;
+        job.g[8] = f->acc_pi;
+        mode = stage == 4 ? D4_RK4 : D4_RK23;
+        ca = stage == 2 ? c.half_dt : (stage == 3 ? c.dt : c.dt6);
+    }
+    return launch_d4(mode, &job, 1, c.lap, ca, 0.0, p, as_stream(stream));
+}
+
+int sb_rhs24(const sb_array *in, const sb_array *out, sb_space space, sb_d4_constants k, sb_poly poly, sb_launch p,
+             void *stream) {
+    if (!in || !out) return fail(SB_USAGE, "rhs24: null array table");
+    int rc;
+    for (int v = 0; v < SB_N_VARS; ++v) {
+        if ((rc = check_array(in[v], 2, "rhs24 in")) || (rc = check_space(space, in[v], "rhs24 in"))) return rc;
+        if ((rc = check_array(out[v], 0, "rhs24 out")) || (rc = check_space(space, out[v], "rhs24 out"))) return rc;
+    }
+    return launch_rhs24(in, out, space, k, poly, p, as_stream(stream));
+}
+
+int sb_copy_h2d(sb_array dst, const double *host, int32_t with_ghosts, void *stream) {
+    int rc = check_array(dst, 0, "copy_h2d");
+    if (rc) return rc;
+    if (!host) return fail(SB_USAGE, "copy_h2d: null host pointer");
+    const int g = with_ghosts ? dst.ghost : 0;
+    const size_t w = (size_t)(dst.nx + 2 * g), rows_y = (size_t)(dst.ny + 2 * g), planes = (size_t)(dst.nz + 2 * g);
+    double *d0 = dst.origin - g - (int64_t)g * dst.sy - (int64_t)g * dst.sz;
+    if (dst.sz == dst.sy * (int64_t)(dst.ny + 2 * dst.ghost) && g == dst.ghost) {
+        // planes are back to back: one 2-D copy of all rows
+        return check_cuda(cudaMemcpy2DAsync(d0, dst.sy * 8, host, w * 8, w * 8, rows_y * planes,
+                                            cudaMemcpyHostToDevice, as_stream(stream)),
+                          "cudaMemcpy2DAsync h2d");
+    }
+    for (size_t z = 0; z < planes; ++z) {
+        rc = check_cuda(cudaMemcpy2DAsync(d0 + z * dst.sz, dst.sy * 8, host + z * rows_y * w, w * 8, w * 8, rows_y,
+                                          cudaMemcpyHostToDevice, as_stream(stream)),
+                        "cudaMemcpy2DAsync h2d");
+        if (rc) return rc;
+    }
+    return SB_OK;
+}
+
+int sb_copy_d2h(double *host, sb_array src, int32_t with_ghosts, void *stream) {
+    int rc = check_array(src, 0, "copy_d2h");
+    if (rc) return rc;
+    if (!host) return fail(SB_USAGE, "copy_d2h: null host pointer");
+    const int g = with_ghosts ? src.ghost : 0;
+    const size_t w = (size_t)(src.nx + 2 * g), rows_y = (size_t)(src.ny + 2 * g), planes = (size_t)(src.nz + 2 * g);
+    const double *s0 = src.origin - g - (int64_t)g * src.sy - (int64_t)g * src.sz;
+    if (src.sz == src.sy * (int64_t)(src.ny + 2 * src.ghost) && g == src.ghost) {
+        return check_cuda(cudaMemcpy2DAsync(host, w * 8, s0, src.sy * 8, w * 8, rows_y * planes,
+                                            cudaMemcpyDeviceToHost, as_stream(stream)),
+                          "cudaMemcpy2DAsync d2h");
+    }
+    for (size_t z = 0; z < planes; ++z) {
+        rc = check_cuda(cudaMemcpy2DAsync(host + z * rows_y * w, w * 8, s0 + z * src.sz, src.sy * 8, w * 8, rows_y,
+                                          cudaMemcpyDeviceToHost, as_stream(stream)),
+                        "cudaMemcpy2DAsync d2h");
+        if (rc) return rc;
+    }
+    return SB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,43 @@
+// internal.h — host-side declarations shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "../../include/stencil_b200.h"
+
+namespace sb {
+
+// Thread-local last-error message + status helpers (abi.cu).
+int fail(int code, const std::string &msg);
+int check_cuda(cudaError_t e, const char *what);
+
+// Build a 3-D tiled TMA descriptor over the ghosted grid `a` whose boxes are
+// (bx, by, bz) elements.  Coordinates of interior (0,0,0) in the map are
+// (a.xpad, a.ghost, a.ghost).
+int make_tmap(CUtensorMap *m, const sb_array &a, int bx, int by, int bz);
+
+// Launchers (one per kernel family, defined next to their kernels).
+int launch_lap7(const sb_array &dst, const sb_array &src, const sb_space &sp, double c0, double c1,
+                const sb_launch &p, cudaStream_t st);
+int launch_diff1d(int kind, double *dst, const double *src, int n, cudaStream_t st);
+
+enum D4Mode { D4_ALL10 = 0, D4_LAP4 = 1, D4_RK1 = 2, D4_RK23 = 3, D4_RK4 = 4 };
+
+struct D4Job {
+    sb_array src;         // stencil input (ghost >= 2)
+    sb_space space;       // region to update
+    sb_array g[10];       // mode-dependent outputs / pointwise inputs
+};
+
+int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, double ca, double cb,
+              const sb_launch &p, cudaStream_t st);
+
+int launch_ghost_periodic(const sb_array &a, cudaStream_t st);
+
+int launch_rhs24(const sb_array *in, const sb_array *out, const sb_space &sp, const sb_d4_constants &k,
+                 const sb_poly &poly, const sb_launch &p, cudaStream_t st);
+
+}  // namespace sb

@@ -1,0 +1,263 @@
+"""Device stencil kernels behind the reference's ``Kernel`` plugin type.
+
+The reference plugs arithmetic into its loop iterator as
+``Kernel = Callable[[IndexSpace], None]`` (traverse.py:159), e.g.
+``_piece_kernel(dst, src)`` around ``_update_rows`` (stencil.py:31-46).
+Each class here is such a callable — ``kernel(piece)`` launches the B200
+kernel over that piece, so the reference's ``execute_plan``/``run_static``
+drive it unchanged — and additionally exposes the fast path the device
+engine uses: ``launch(space, params)`` covers a whole index space (or a
+whole level) in one launch with a :class:`~.tuner.LaunchParams` tile shape,
+and ``launch_space()`` names the tunable space for the GPU tuner.
+
+Index spaces are in the caller's coordinates; each kernel subtracts the
+grid's ``lower`` (so the reference's array-index pieces work for the demo,
+and level coordinates work for bboxset boxes).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .errors import UsageError
+from .grid import DeviceGrid, stream_ptr
+from .inputs import N_TERMS, N_VARS, D4Constants, PolyTable, WaveConstants
+from .traverse import IndexSpace
+from .tuner import LaunchParams, LaunchSpace
+
+D4_ALL_SPACE = LaunchSpace(kind="d4_all", max_threads=256, rx_buffer=True)
+D4_SPACE = LaunchSpace(kind="d4", max_threads=512)
+LAP7_SPACE = LaunchSpace(kind="lap7", max_threads=256, radius=1, stages=0, tile_xs=(64,), tile_ys=(1, 2, 4, 8))
+
+
+def _local(space: IndexSpace, grid: DeviceGrid) -> _lib.sb_space:
+    if space.dim != 3:
+        raise UsageError("device stencil kernels sweep 3-D index spaces")
+    lo = tuple(a - o for a, o in zip(space.lo, grid.lower))
+    hi = tuple(b - o for b, o in zip(space.hi, grid.lower))
+    return _lib.space(lo, hi)
+
+
+def _interior_space(grid: DeviceGrid) -> IndexSpace:
+    return IndexSpace(grid.lower, tuple(l + e for l, e in zip(grid.lower, grid.extents)))
+
+
+class DeviceKernel:
+    """Common behaviour of the device kernels (plugin + fast path)."""
+
+    site_id = "kernel"
+    space_kind = D4_SPACE
+    default_params: LaunchParams = LaunchParams(64, 8, 32)
+
+    def launch_space(self) -> LaunchSpace:
+        return self.space_kind
+
+    def __call__(self, piece: IndexSpace) -> None:
+        self.launch(piece, self.default_params)
+
+    def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
+        raise NotImplementedError
+
+    def full_space(self) -> IndexSpace:
+        raise NotImplementedError
+
+
+class Laplacian7(DeviceKernel):
+    """K1 — ``_update_rows`` (stencil.py:31-39): dst = C0*b + C1*(sum of 6 neighbours)."""
+
+    site_id = "laplacian3d"
+    space_kind = LAP7_SPACE
+    default_params = LaunchParams(64, 8, 16)
+
+    def __init__(self, dst: DeviceGrid, src: DeviceGrid, c0: float, c1: float):
+        if src.ghost < 1:
+            raise UsageError("7-point stencil needs ghost width >= 1")
+        if dst.lower != src.lower or dst.extents != src.extents:
+            raise UsageError("dst and src must cover the same box")
+        self.dst, self.src, self.c0, self.c1 = dst, src, float(c0), float(c1)
+
+    def full_space(self) -> IndexSpace:
+        return _interior_space(self.src)
+
+    def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
+        _lib.call("sb_lap7", self.dst.abi(), self.src.abi(), _local(space, self.src), self.c0, self.c1,
+                  _lib.launch(params.tile_x, params.tile_y, params.z_chunk), stream_ptr(stream))
+
+
+class FourthOrderAll(DeviceKernel):
+    """K2 — all ten 4th-order outputs of a box (config 2): Dx Dy Dz Dxx Dyy Dzz Dxy Dxz Dyz Lap4."""
+
+    site_id = "d4_all"
+    space_kind = D4_ALL_SPACE
+    default_params = LaunchParams(64, 4, 32)
+
+    def __init__(self, outs: list[DeviceGrid], src: DeviceGrid, k: D4Constants):
+        if len(outs) != _lib.SB_N_D4_OUT:
+            raise UsageError("need 10 output grids")
+        if src.ghost < 2:
+            raise UsageError("4th-order stencils need ghost width >= 2")
+        self.outs, self.src, self.k = list(outs), src, k
+        self._out_abi = (_lib.sb_array * 10)(*[o.abi() for o in self.outs])
+
+    def full_space(self) -> IndexSpace:
+        return _interior_space(self.src)
+
+    def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
+        _lib.call("sb_d4_all", self._out_abi, self.src.abi(), _local(space, self.src), _lib.d4_constants(self.k),
+                  _lib.launch(params.tile_x, params.tile_y, params.z_chunk), stream_ptr(stream))
+
+
+class Laplacian4(DeviceKernel):
+    """K3 — 4th-order Laplacian of one box; see :class:`LevelLaplacian4` for levels."""
+
+    site_id = "lap4"
+    space_kind = D4_SPACE
+    default_params = LaunchParams(64, 8, 32)
+
+    def __init__(self, dst: DeviceGrid, src: DeviceGrid, k: D4Constants):
+        if src.ghost < 2:
+            raise UsageError("4th-order stencils need ghost width >= 2")
+        self.dst, self.src, self.k = dst, src, k
+
+    def full_space(self) -> IndexSpace:
+        return _interior_space(self.src)
+
+    def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
+        job = _lib.sb_box_job(self.dst.abi(), self.src.abi(), _local(space, self.src))
+        _lib.call("sb_lap4_boxes", C.byref(job), 1, _lib.d4_constants(self.k),
+                  _lib.launch(params.tile_x, params.tile_y, params.z_chunk), stream_ptr(stream))
+
+
+class LevelLaplacian4(DeviceKernel):
+    """K3 over a whole refinement level: every box in ONE launch through the
+    device box table (blockIdx -> (box, tile)).  ``launch`` ignores the space
+    argument's extent and sweeps each box's interior; ``__call__(piece)``
+    sweeps the part of ``piece`` inside each box (level coordinates)."""
+
+    site_id = "lap4_level"
+    space_kind = D4_SPACE
+    default_params = LaunchParams(64, 8, 32)
+
+    def __init__(self, dsts: list[DeviceGrid], srcs: list[DeviceGrid], k: D4Constants):
+        if len(dsts) != len(srcs) or not srcs:
+            raise UsageError("need one dst per src box")
+        for s in srcs:
+            if s.ghost < 2:
+                raise UsageError("4th-order stencils need ghost width >= 2")
+        self.dsts, self.srcs, self.k = list(dsts), list(srcs), k
+
+    def full_space(self) -> IndexSpace:
+        lo = tuple(min(s.lower[d] for s in self.srcs) for d in range(3))
+        hi = tuple(max(s.lower[d] + s.extents[d] for s in self.srcs) for d in range(3))
+        return IndexSpace(lo, hi)
+
+    def _jobs(self, space: IndexSpace | None):
+        jobs = []
+        for d, s in zip(self.dsts, self.srcs):
+            box = _interior_space(s)
+            if space is not None:
+                lo = tuple(max(a, b) for a, b in zip(box.lo, space.lo))
+                hi = tuple(min(a, b) for a, b in zip(box.hi, space.hi))
+                if any(h <= l for l, h in zip(lo, hi)):
+                    continue
+                box = IndexSpace(lo, hi)
+            jobs.append(_lib.sb_box_job(d.abi(), s.abi(), _local(box, s)))
+        return jobs
+
+    def _run(self, jobs, params, stream) -> None:
+        for i in range(0, len(jobs), _lib.SB_MAX_BOXES):
+            chunk = jobs[i:i + _lib.SB_MAX_BOXES]
+            arr = (_lib.sb_box_job * len(chunk))(*chunk)
+            _lib.call("sb_lap4_boxes", arr, len(chunk), _lib.d4_constants(self.k),
+                      _lib.launch(params.tile_x, params.tile_y, params.z_chunk), stream_ptr(stream))
+
+    def launch(self, space: IndexSpace | None, params: LaunchParams, stream=None) -> None:
+        self._run(self._jobs(None if space is None else space), params, stream)
+
+    def __call__(self, piece: IndexSpace) -> None:
+        self._run(self._jobs(piece), self.default_params, None)
+
+
+class PeriodicGhosts:
+    """K4 — periodic refill of a grid's ghost shell."""
+
+    def __init__(self, grid: DeviceGrid):
+        self.grid = grid
+
+    def __call__(self, stream=None) -> None:
+        _lib.call("sb_ghost_periodic", self.grid.abi(), stream_ptr(stream))
+
+
+class WaveRK4:
+    """K4 + K5 — one classical RK4 step of d/dt(phi, pi) = (pi, Lap4 phi) on a
+    periodic box: four stage launches, each preceded by a periodic ghost
+    refill of the stage's phi.  State buffers are allocated once."""
+
+    site_id = "wave_rk4"
+
+    def __init__(self, n: int, ghost: int, c: WaveConstants, device=None):
+        self.n, self.g, self.c = n, ghost, c
+        mk = lambda: DeviceGrid((n, n, n), ghost, device)
+        self.phi0, self.pi0 = mk(), mk()
+        self.phi_a, self.pi_a, self.phi_b, self.pi_b = mk(), mk(), mk(), mk()
+        self.acc_phi, self.acc_pi = mk(), mk()
+        self.params = LaunchParams(64, 8, 32)
+
+    def _consts(self) -> _lib.sb_rk4_constants:
+        return _lib.sb_rk4_constants(_lib.d4_constants(self.c.lap), self.c.half_dt, self.c.dt, self.c.dt6)
+
+    def stage(self, s: int, phi_s: DeviceGrid, pi_s: DeviceGrid, phi_out: DeviceGrid, pi_out: DeviceGrid,
+              params: LaunchParams, stream=None) -> None:
+        _lib.call("sb_ghost_periodic", phi_s.abi(), stream_ptr(stream))
+        f = _lib.sb_rk4_fields(phi_s.abi(), pi_s.abi(), self.phi0.abi(), self.pi0.abi(), self.acc_phi.abi(),
+                               self.acc_pi.abi(), phi_out.abi(), pi_out.abi())
+        n = self.n
+        _lib.call("sb_rk4_stage", s, C.byref(f), _lib.space((0, 0, 0), (n, n, n)), self._consts(),
+                  _lib.launch(params.tile_x, params.tile_y, params.z_chunk), stream_ptr(stream))
+
+    def step(self, params: LaunchParams | None = None, stream=None) -> tuple[DeviceGrid, DeviceGrid]:
+        """One RK4 step from (phi0, pi0); returns the grids holding the new state
+        (phi0/pi0 themselves are left unchanged)."""
+        p = params or self.params
+        self.stage(1, self.phi0, self.pi0, self.phi_a, self.pi_a, p, stream)
+        self.stage(2, self.phi_a, self.pi_a, self.phi_b, self.pi_b, p, stream)
+        self.stage(3, self.phi_b, self.pi_b, self.phi_a, self.pi_a, p, stream)
+        self.stage(4, self.phi_a, self.pi_a, self.phi_b, self.pi_b, p, stream)
+        return self.phi_b, self.pi_b
+
+    def advance(self, params: LaunchParams | None = None, stream=None) -> None:
+        """Step and make the new state the start of the next step."""
+        phi, pi = self.step(params, stream)
+        self.phi0, self.phi_b = phi, self.phi0
+        self.pi0, self.pi_b = pi, self.pi0
+
+
+class Rhs24(DeviceKernel):
+    """K6 — config-5 fused 24-variable right-hand side."""
+
+    site_id = "rhs24"
+    space_kind = LaunchSpace(kind="rhs24", max_threads=512, tile_xs=(32, 64, 128))
+    default_params = LaunchParams(64, 8, 32)   # fixed 8x4x2 point blocks; params unused
+
+    def __init__(self, ins: list[DeviceGrid], outs: list[DeviceGrid], k: D4Constants, poly: PolyTable):
+        if len(ins) != N_VARS or len(outs) != N_VARS:
+            raise UsageError("need 24 input and 24 output grids")
+        for g in ins:
+            if g.ghost < 2:
+                raise UsageError("4th-order stencils need ghost width >= 2")
+        self.ins, self.outs, self.k = list(ins), list(outs), k
+        self._coef = np.ascontiguousarray(poly.coef, dtype=np.float64).reshape(N_VARS * N_TERMS)
+        self._p = np.ascontiguousarray(poly.p, dtype=np.int32).reshape(-1)
+        self._q = np.ascontiguousarray(poly.q, dtype=np.int32).reshape(-1)
+        self._in = (_lib.sb_array * N_VARS)(*[g.abi() for g in self.ins])
+        self._out = (_lib.sb_array * N_VARS)(*[g.abi() for g in self.outs])
+
+    def full_space(self) -> IndexSpace:
+        return _interior_space(self.ins[0])
+
+    def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
+        poly = _lib.sb_poly(self._coef.ctypes.data, self._p.ctypes.data, self._q.ctypes.data)
+        _lib.call("sb_rhs24", self._in, self._out, _local(space, self.ins[0]), _lib.d4_constants(self.k), poly,
+                  _lib.launch(params.tile_x, params.tile_y, params.z_chunk), stream_ptr(stream))

@@ -1,0 +1,113 @@
+"""Refinement levels as box lists, and the device box table.
+
+The reference represents a level as a ``BBoxSet`` (bboxset.py) and hands the
+loop iterator one box at a time through ``index_space_from_bbox``
+(traverse.py:59-65).  The hot path only needs the level's canonical disjoint
+decomposition, ``BBoxSet.from_bboxes(...).difference(...).to_bboxes()``
+(bboxset.py:259-294, 352-353, 313-317); the set algebra itself is host-side
+integer logic and out of scope.
+
+:func:`boxes_of` accepts any object with ``to_bboxes()`` (the reference's
+``BBoxSet``), a list of reference ``BBox`` objects, or a list of :class:`Box`.
+:func:`box_difference` produces, for the single-box-minus-box case config 4
+uses, the same sorted slab decomposition the reference returns (outermost
+dimension split first; verified against the reference in
+tests/golden/make_golden.py).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from .errors import UsageError
+
+
+@dataclass(frozen=True)
+class _Pt:
+    coords: tuple[int, ...]
+
+
+@dataclass(frozen=True)
+class Box:
+    """Inclusive, unit-stride box, innermost dimension first (lattice.py:104)."""
+
+    lo: tuple[int, ...]
+    hi: tuple[int, ...]
+
+    @staticmethod
+    def empty(dim: int) -> "Box":
+        return Box((0,) * dim, (-1,) * dim)
+
+    @property
+    def is_empty(self) -> bool:
+        return any(h < l for l, h in zip(self.lo, self.hi))
+
+    @property
+    def dim(self) -> int:
+        return len(self.lo)
+
+    # duck-typing with the reference's BBox
+    @property
+    def lower(self):
+        return _Pt(self.lo)
+
+    @property
+    def upper(self):
+        return _Pt(self.hi)
+
+    @property
+    def stride(self):
+        return _Pt((1,) * self.dim)
+
+    @property
+    def extents(self) -> tuple[int, ...]:
+        return tuple(max(0, h - l + 1) for l, h in zip(self.lo, self.hi))
+
+    def volume(self) -> int:
+        v = 1
+        for e in self.extents:
+            v *= e
+        return v
+
+
+def as_box(b) -> Box:
+    if isinstance(b, Box):
+        return b
+    lower = tuple(b.lower.coords)
+    upper = tuple(b.upper.coords)
+    if b.is_empty:
+        return Box.empty(len(lower))
+    if any(s != 1 for s in b.stride.steps):
+        raise UsageError("only unit-stride boxes can be swept")
+    return Box(lower, upper)
+
+
+def boxes_of(level) -> list[Box]:
+    """Canonical box list of a level: ``level.to_bboxes()`` or an iterable."""
+    raw = level.to_bboxes() if hasattr(level, "to_bboxes") else list(level)
+    return [b for b in (as_box(x) for x in raw) if not b.is_empty]
+
+
+def box_difference(a: Box, b: Box) -> list[Box]:
+    """Disjoint boxes covering a \\ b, split outermost dimension first, sorted by
+    (lower, upper) compared outermost-first — the order of the reference's
+    ``to_bboxes`` for this case."""
+    if a.is_empty:
+        return []
+    lo = [max(x, y) for x, y in zip(a.lo, b.lo)]
+    hi = [min(x, y) for x, y in zip(a.hi, b.hi)]
+    if b.is_empty or any(h < l for l, h in zip(lo, hi)):
+        return [a]
+    pieces = []
+    cur_lo, cur_hi = list(a.lo), list(a.hi)
+    for d in reversed(range(a.dim)):            # outermost first
+        if cur_lo[d] < lo[d]:
+            p_hi = list(cur_hi)
+            p_hi[d] = lo[d] - 1
+            pieces.append(Box(tuple(cur_lo), tuple(p_hi)))
+        if hi[d] < cur_hi[d]:
+            p_lo = list(cur_lo)
+            p_lo[d] = hi[d] + 1
+            pieces.append(Box(tuple(p_lo), tuple(cur_hi)))
+        cur_lo[d], cur_hi[d] = lo[d], hi[d]
+    key = lambda bx: (tuple(reversed(bx.lo)), tuple(reversed(bx.hi)))
+    return sorted(pieces, key=key)

@@ -1,0 +1,93 @@
+"""The reference's stencil demo, running on the B200.
+
+Same drivers and semantics as ``pkg/src/stencilrt/stencil.py``: a Jacobi
+7-point update per iteration, boundary carried over, run serially
+(:55-65), with the naive static split (:68-77) and tuned (:80-94), and the
+``bit_identical`` predicate (:97-98).  The field is generated on the host
+(``make_field``, :26-28) and uploaded once; the two device buffers ping-pong
+(``dst = src.copy()`` at :59 only carries the boundary over, which the
+second buffer already holds), and ``iter_seconds`` are CUDA-event times of
+the sweep.  Index spaces are the reference's array indices
+``IndexSpace((1,1,1), (n-1,n-1,n-1))``.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .grid import DeviceGrid
+from .kernels import Laplacian7
+from .traverse import IndexSpace, _Timer, run_loop, run_static
+from .tuner import LoopSetup, TopologyConfig, Tuner
+
+C0 = -6.0 / 8.0
+C1 = 1.0 / 8.0
+
+
+def make_field(n: int, seed: int) -> np.ndarray:
+    """stencil.py:26-28."""
+    return np.random.default_rng(seed).random((n, n, n), dtype=np.float64)
+
+
+@dataclass
+class StencilRun:
+    final: np.ndarray
+    iter_seconds: list[float] = field(default_factory=list)
+
+
+def _buffers(n: int, seed: int):
+    host = make_field(n, seed)
+    a = DeviceGrid((n - 2,) * 3, 1, lower=(1, 1, 1))
+    b = DeviceGrid((n - 2,) * 3, 1, lower=(1, 1, 1))
+    a.upload(host, with_ghosts=True)
+    b.upload(host, with_ghosts=True)
+    return a, b
+
+
+def _space(n: int) -> IndexSpace:
+    return IndexSpace((1, 1, 1), (n - 1, n - 1, n - 1))
+
+
+def run_serial(n: int, iters: int, seed: int, c0: float = C0, c1: float = C1) -> StencilRun:
+    src, dst = _buffers(n, seed)
+    out = StencilRun(np.empty(0))
+    space = _space(n)
+    for _ in range(iters):
+        k = Laplacian7(dst, src, c0, c1)
+        with _Timer(True) as tm:
+            k.launch(space, k.default_params)
+        out.iter_seconds.append(tm.elapsed())
+        src, dst = dst, src
+    out.final = src.download(with_ghosts=True)
+    return out
+
+
+def run_naive(n: int, iters: int, seed: int, n_threads: int, c0: float = C0, c1: float = C1) -> StencilRun:
+    src, dst = _buffers(n, seed)
+    out = StencilRun(np.empty(0))
+    space = _space(n)
+    for _ in range(iters):
+        out.iter_seconds.append(run_static(space, Laplacian7(dst, src, c0, c1), n_threads))
+        src, dst = dst, src
+    out.final = src.download(with_ghosts=True)
+    return out
+
+
+def run_tuned(n: int, iters: int, seed: int, topo: TopologyConfig, c0: float = C0,
+              c1: float = C1) -> tuple[StencilRun, Tuner]:
+    src, dst = _buffers(n, seed)
+    out = StencilRun(np.empty(0))
+    space = _space(n)
+    setup = LoopSetup("laplacian3d", space.extents, "vector", topo.n_coarse_threads, topo.n_fine_threads)
+    tuner = Tuner(topo)
+    for _ in range(iters):
+        out.iter_seconds.append(run_loop(setup, space, Laplacian7(dst, src, c0, c1), tuner))
+        src, dst = dst, src
+    out.final = src.download(with_ghosts=True)
+    return out, tuner
+
+
+def bit_identical(a: np.ndarray, b: np.ndarray) -> bool:
+    """stencil.py:97-98."""
+    return a.shape == b.shape and a.tobytes() == b.tobytes()
