@@ -78,14 +78,18 @@ typedef struct sb_space {
 } sb_space;
 
 /* One point of the GPU tuning space (the device counterpart of the
- * reference's ExecParams, tuner.py:99-111): CTA tile in x and y, and the
- * number of z planes one CTA streams.  tile_x is a multiple of 32. */
+ * reference's ExecParams, tuner.py:99-111): CTA tile in x and y, the number
+ * of z planes one CTA streams, and whether a thread owns one x point or a
+ * 16-byte pair (the SIMD width W of vlanes.py).  tile_x is 32, 64 or 128. */
 typedef struct sb_launch {
     int32_t tile_x;
     int32_t tile_y;
     int32_t z_chunk;
-    int32_t flags;    /* reserved, 0 */
+    int32_t flags;    /* SB_LAUNCH_* bits */
 } sb_launch;
+
+/* sb_launch.flags: one x point per thread instead of a 16-byte pair. */
+#define SB_LAUNCH_SCALAR 1
 
 /* 4th-order constants: k1 = 1/(12h), k2 = 1/(12h^2), k11 = 1/(144h^2). */
 typedef struct sb_d4_constants {

@@ -133,8 +133,17 @@ def space(lo, hi) -> sb_space:
     return s
 
 
-def launch(tile_x: int, tile_y: int, z_chunk: int) -> sb_launch:
-    return sb_launch(int(tile_x), int(tile_y), int(z_chunk), 0)
+SB_LAUNCH_SCALAR = 1
+
+
+def launch(tile_x: int, tile_y: int, z_chunk: int, points_per_thread: int = 2) -> sb_launch:
+    flags = SB_LAUNCH_SCALAR if points_per_thread == 1 else 0
+    return sb_launch(int(tile_x), int(tile_y), int(z_chunk), flags)
+
+
+def launch_of(p) -> sb_launch:
+    """sb_launch of a tuner.LaunchParams."""
+    return launch(p.tile_x, p.tile_y, p.z_chunk, getattr(p, "points_per_thread", 2))
 
 
 def d4_constants(k) -> sb_d4_constants:

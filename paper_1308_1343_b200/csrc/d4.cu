@@ -7,17 +7,19 @@
 //   * blockIdx.x -> (box, tile) through the device box table (tile prefix);
 //   * a CTA owns a TX x TY tile of (x, y) columns and streams z planes
 //     Z0-2 .. Z1+1 (z_chunk = Z1-Z0 output planes);
-//   * one producer warp moves each plane of the tile plus its 2-point halo
-//     (TX+4) x (TY+4) from HBM into a 4-stage shared-memory ring with TMA
-//     (cp.async.bulk.tensor.3d), completion on mbarriers; consumer warps
-//     release a stage with one arrive per warp;
-//   * each consumer thread owns two adjacent x points (double2 loads and
-//     stores, x tiles anchored on absolute multiples of TX so pairs are
-//     16-byte aligned — the iterate_masked frame rule, vlanes.py:322-337:
-//     lanes outside [lo, hi) compute but never store);
+//   * each plane of the tile plus its 2-point halo, (TX+4) x (TY+4), moves
+//     from HBM into a 4-stage shared-memory ring by TMA
+//     (cp.async.bulk.tensor.3d) with mbarrier completion; after the one
+//     CTA barrier per plane (all reads of that stage done) thread 0 re-arms
+//     the stage for plane i+4 — no producer warp, no spinning;
+//   * each thread owns NP (1 or 2) adjacent x points; x tiles are anchored on
+//     absolute multiples of TX, so pairs are 16-byte aligned and lanes outside
+//     [lo, hi) compute but never store (the iterate_masked frame rule,
+//     vlanes.py:322-337);
 //   * in-plane terms (Dx, Dy, Dxx, Dyy, Dxy) come from shared memory; the z
-//     terms (Dz, Dzz, Dxz, Dyz) from per-thread register windows of u, of
-//     the unscaled x/y first differences and of Dxx+Dyy over five planes.
+//     terms (Dz, Dzz, Dxz, Dyz, Lap) from five-slot register rings of u, of the
+//     unscaled x/y first differences and of Dxx+Dyy; the plane loop is
+//     unrolled five ways so ring slots are compile-time registers (no moves).
 //
 // Every expression tree and association matches oracle/stencils.py
 // (SURVEY.md App. A):  d1u = (u[-2]-u[+2]) + 8*(u[+1]-u[-1]),
@@ -34,17 +36,20 @@ namespace sb {
 namespace {
 
 constexpr int kStages = 4;
-// (tile_x/2)*tile_y limit per mode: ALL10 keeps ~36 doubles of z windows per
-// thread (~140 registers), the single-output modes ~75 registers.
-__host__ __device__ constexpr int max_consumers(int mode) { return mode == 0 ? 256 : 512; }
+
+// consumer threads per CTA allowed for (mode, points per thread)
+__host__ __device__ constexpr int max_threads(int mode, int np) {
+    return (np == 2 && mode != D4_LAP4) ? 256 : 512;
+}
 
 struct BoxDesc {
     CUtensorMap tmap;          // plane boxes of (TX+4) x (TY+4) x 1 over the source grid
-    Grid g[10];                // mode-dependent outputs / pointwise inputs
+    double *g[10];             // mode-dependent outputs / pointwise inputs (origins)
+    long long sy, sz;          // strides shared by every g[] of the box
     int tma0[3];               // TMA coordinates of interior (0,0,0)
     int lo[3], hi[3];
     int ax0;                   // x tile anchor: floor(lo.x / TX) * TX
-    int ntx, nty, ntz;
+    int ntx, nty;
     int tile_begin;
 };
 
@@ -53,293 +58,386 @@ struct D4Params {
     int nbox;
     int ty, zc;
     double k1, k2, k11;
-    double ca, cb;
+    double ca;
 };
 
-template <int MODE, int TX>
-__global__ void __launch_bounds__(max_consumers(MODE) + 32, 1) d4_kernel(const __grid_constant__ D4Params P) {
-    constexpr int CPR = TX / 2;     // column pairs per row
-    constexpr int W = TX + 4;       // smem row width (elements)
-    const int TY = P.ty;
-    const int H = TY + 4;
-    const int ncons = CPR * TY;
-    const int stage_elems = round_up(W * H, 16);
+// Predicated streaming stores (no branches): pair / single lanes.
+__device__ __forceinline__ void st_v2(double *p, double a, double b, int pred) {
+    asm volatile(
+        "{\n.reg .pred q;\nsetp.ne.b32 q, %3, 0;\n@q st.global.cs.v2.f64 [%0], {%1, %2};\n}\n" ::"l"(p), "d"(a),
+        "d"(b), "r"(pred)
+        : "memory");
+}
+__device__ __forceinline__ void st_1(double *p, double a, int pred) {
+    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.global.cs.f64 [%0], %1;\n}\n" ::"l"(p), "d"(a),
+                 "r"(pred)
+                 : "memory");
+}
 
+template <int NP>
+struct Lanes {
+    int m[NP];           // per-point store masks
+    int full, only0, only1;  // NP == 2 store classes
+};
+
+template <int NP>
+__device__ __forceinline__ void store(double *p, const double (&v)[NP], const Lanes<NP> &L) {
+    if constexpr (NP == 2) {
+        st_v2(p, v[0], v[1], L.full);
+        st_1(p, v[0], L.only0);
+        st_1(p + 1, v[1], L.only1);
+    } else {
+        st_1(p, v[0], L.m[0]);
+    }
+}
+
+template <int NP>
+__device__ __forceinline__ void load(const double *p, double (&v)[NP], const Lanes<NP> &L) {
+    if constexpr (NP == 2) {
+        if (L.full) {
+            const double2 t = load_pair(p);
+            v[0] = t.x;
+            v[1] = t.y;
+        } else {
+            v[0] = L.m[0] ? p[0] : 0.0;
+            v[1] = L.m[1] ? p[1] : 0.0;
+        }
+    } else {
+        v[0] = L.m[0] ? p[0] : 0.0;
+    }
+}
+
+// Row values x-2 .. x+NP+1 of shared-memory row `r` starting at column c (= x-2).
+template <int NP>
+__device__ __forceinline__ void row_vals(const double *r, double (&v)[NP + 4]) {
+    if constexpr (NP == 2) {
+        const double2 a = load_pair(r), b = load_pair(r + 2), c = load_pair(r + 4);
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = c.x; v[5] = c.y;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) v[k] = r[k];
+    }
+}
+
+template <int NP>
+__device__ __forceinline__ void col_vals(const double *r, double (&v)[NP]) {
+    if constexpr (NP == 2) {
+        const double2 a = load_pair(r);
+        v[0] = a.x; v[1] = a.y;
+    } else {
+        v[0] = r[0];
+    }
+}
+
+template <int NP>
+struct Rings {
+    double u[5][NP], s[5][NP], rx[5][NP], ry[5][NP];
+};
+
+struct Ctx {
+    const double *stages;
+    double *rxb;
+    uint64_t *full;
+    int stage_elems, H, TY, nthr, tid, cx, ry;
+    int X0, Y0, Z0, Z1, nplanes;
+    long long off_xy;   // x + y*sy of the thread's first point
+};
+
+template <int MODE, int TX, int NP, int R>
+__device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &P, const BoxDesc &B,
+                                           const Lanes<NP> &L, Rings<NP> &rg) {
+    constexpr int W = TX + 4;
+    if (i >= c.nplanes) return true;
+    const int s = i & (kStages - 1);
+    const int z = c.Z0 - 2 + i;    // plane held by this stage
+    const int zc = z - 2;          // plane whose z terms complete now (i >= 4)
+    const long long offc = c.off_xy + (long long)zc * B.sz;
+
+    // pointwise operands of the RK stages for plane zc, issued before the wait
+    double pw[5][NP];
+    if constexpr (MODE >= D4_RK1) {
+        if (i >= 4) {
+            constexpr int np = (MODE == D4_RK1) ? 1 : 5;
+#pragma unroll
+            for (int a = 0; a < np; ++a) load<NP>(B.g[4 + a] + offc, pw[a], L);
+        }
+    }
+
+    mbar_wait(&c.full[s], (i / kStages) & 1);
+    const double *pl = c.stages + s * c.stage_elems;
+    double xr[NP + 4], ym2[NP], ym1[NP], yp1[NP], yp2[NP];
+    row_vals<NP>(pl + (c.ry + 2) * W + NP * c.cx, xr);
+    col_vals<NP>(pl + (c.ry + 0) * W + NP * c.cx + 2, ym2);
+    col_vals<NP>(pl + (c.ry + 1) * W + NP * c.cx + 2, ym1);
+    col_vals<NP>(pl + (c.ry + 3) * W + NP * c.cx + 2, yp1);
+    col_vals<NP>(pl + (c.ry + 4) * W + NP * c.cx + 2, yp2);
+
+    double rx[NP], ryv[NP];
+    double *rxs = c.rxb + (i & 1) * c.H * TX;
+    if constexpr (MODE == D4_ALL10) {
+        // unscaled x differences of this thread's share of the 4 halo rows
+        for (int h = c.ry; h < 4; h += c.TY) {
+            const int hr = h < 2 ? h : c.TY + h;
+            double hv[NP + 4];
+            row_vals<NP>(pl + hr * W + NP * c.cx, hv);
+            double r[NP];
+#pragma unroll
+            for (int j = 0; j < NP; ++j) r[j] = d1u(hv[j], hv[j + 1], hv[j + 3], hv[j + 4]);
+            if constexpr (NP == 2)
+                *reinterpret_cast<double2 *>(rxs + hr * TX + 2 * c.cx) = make_double2(r[0], r[1]);
+            else
+                rxs[hr * TX + c.cx] = r[0];
+        }
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            rx[j] = d1u(xr[j], xr[j + 1], xr[j + 3], xr[j + 4]);
+            ryv[j] = d1u(ym2[j], ym1[j], yp1[j], yp2[j]);
+        }
+        if constexpr (NP == 2)
+            *reinterpret_cast<double2 *>(rxs + (c.ry + 2) * TX + 2 * c.cx) = make_double2(rx[0], rx[1]);
+        else
+            rxs[(c.ry + 2) * TX + c.cx] = rx[0];
+    }
+    double dxx[NP], dyy[NP];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+        dxx[j] = d2(xr[j], xr[j + 1], xr[j + 2], xr[j + 3], xr[j + 4], P.k2);
+        dyy[j] = d2(ym2[j], ym1[j], xr[j + 2], yp1[j], yp2[j], P.k2);
+        rg.u[R][j] = xr[j + 2];
+        rg.s[R][j] = add(dxx[j], dyy[j]);
+        if constexpr (MODE == D4_ALL10) {
+            rg.rx[R][j] = rx[j];
+            rg.ry[R][j] = ryv[j];
+        }
+    }
+
+    // every thread is done with stage s (and rx of this plane is visible)
+    named_bar(1, c.nthr);
+    if (c.tid == 0 && i + kStages < c.nplanes) {
+        mbar_arrive_expect_tx(&c.full[s], (uint32_t)(W * c.H * 8));
+        tma_load_3d(const_cast<double *>(pl), &B.tmap, B.tma0[0] + c.X0 - 2, B.tma0[1] + c.Y0 - 2,
+                    B.tma0[2] + c.Z0 - 2 + i + kStages, &c.full[s]);
+    }
+
+    if constexpr (MODE == D4_ALL10) {
+        if (z >= c.Z0 && z < c.Z1) {
+            double r_m2[NP], r_m1[NP], r_p1[NP], r_p2[NP];
+            const double *rc = rxs + NP * c.cx;
+            col_vals<NP>(rc + (c.ry + 0) * TX, r_m2);
+            col_vals<NP>(rc + (c.ry + 1) * TX, r_m1);
+            col_vals<NP>(rc + (c.ry + 3) * TX, r_p1);
+            col_vals<NP>(rc + (c.ry + 4) * TX, r_p2);
+            const long long off = c.off_xy + (long long)z * B.sz;
+            double o[NP];
+#pragma unroll
+            for (int j = 0; j < NP; ++j) o[j] = mul(rx[j], P.k1);
+            store<NP>(B.g[0] + off, o, L);
+#pragma unroll
+            for (int j = 0; j < NP; ++j) o[j] = mul(ryv[j], P.k1);
+            store<NP>(B.g[1] + off, o, L);
+            store<NP>(B.g[3] + off, dxx, L);
+            store<NP>(B.g[4] + off, dyy, L);
+#pragma unroll
+            for (int j = 0; j < NP; ++j) o[j] = mul(d1u(r_m2[j], r_m1[j], r_p1[j], r_p2[j]), P.k11);
+            store<NP>(B.g[6] + off, o, L);
+        }
+    }
+
+    if (i < 4) return false;
+
+    // ---- plane zc: ring slot of logical window position k is (R + 1 + k) % 5 ----
+    constexpr int K0 = (R + 1) % 5, K1 = (R + 2) % 5, K2 = (R + 3) % 5, K3 = (R + 4) % 5, K4 = R;
+    double dzz[NP], lap[NP];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+        dzz[j] = d2(rg.u[K0][j], rg.u[K1][j], rg.u[K2][j], rg.u[K3][j], rg.u[K4][j], P.k2);
+        lap[j] = add(rg.s[K2][j], dzz[j]);
+    }
+    if constexpr (MODE == D4_ALL10) {
+        double o[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) o[j] = mul(d1u(rg.u[K0][j], rg.u[K1][j], rg.u[K3][j], rg.u[K4][j]), P.k1);
+        store<NP>(B.g[2] + offc, o, L);
+        store<NP>(B.g[5] + offc, dzz, L);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) o[j] = mul(d1u(rg.rx[K0][j], rg.rx[K1][j], rg.rx[K3][j], rg.rx[K4][j]), P.k11);
+        store<NP>(B.g[7] + offc, o, L);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) o[j] = mul(d1u(rg.ry[K0][j], rg.ry[K1][j], rg.ry[K3][j], rg.ry[K4][j]), P.k11);
+        store<NP>(B.g[8] + offc, o, L);
+        store<NP>(B.g[9] + offc, lap, L);
+    } else if constexpr (MODE == D4_LAP4) {
+        store<NP>(B.g[0] + offc, lap, L);
+    } else if constexpr (MODE == D4_RK1) {
+        // k1 = (pi0, L(phi0)); phi2 = phi0 + (dt/2) pi0; pi2 = pi0 + (dt/2) L; acc = k1
+        const double cc = P.ca;
+        double fo[NP], po[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            fo[j] = add(rg.u[K2][j], mul(cc, pw[0][j]));
+            po[j] = add(pw[0][j], mul(cc, lap[j]));
+        }
+        store<NP>(B.g[0] + offc, fo, L);
+        store<NP>(B.g[1] + offc, po, L);
+        store<NP>(B.g[2] + offc, pw[0], L);
+        store<NP>(B.g[3] + offc, lap, L);
+    } else {
+        // pw: 0 pi_s, 1 phi0, 2 pi0, 3 acc_phi, 4 acc_pi
+        const double cc = P.ca;
+        double o0[NP], o1[NP];
+        if constexpr (MODE == D4_RK23) {
+            double o2[NP], o3[NP];
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                o0[j] = add(pw[1][j], mul(cc, pw[0][j]));
+                o1[j] = add(pw[2][j], mul(cc, lap[j]));
+                o2[j] = add(pw[3][j], mul(2.0, pw[0][j]));
+                o3[j] = add(pw[4][j], mul(2.0, lap[j]));
+            }
+            store<NP>(B.g[2] + offc, o2, L);
+            store<NP>(B.g[3] + offc, o3, L);
+        } else {
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                o0[j] = add(pw[1][j], mul(cc, add(pw[3][j], pw[0][j])));
+                o1[j] = add(pw[2][j], mul(cc, add(pw[4][j], lap[j])));
+            }
+        }
+        store<NP>(B.g[0] + offc, o0, L);
+        store<NP>(B.g[1] + offc, o1, L);
+    }
+    return false;
+}
+
+template <int MODE, int TX, int NP>
+__global__ void __launch_bounds__(max_threads(MODE, NP), 1) d4_kernel(const __grid_constant__ D4Params P) {
+    constexpr int TPR = TX / NP;    // threads per row
+    constexpr int W = TX + 4;       // smem row width (elements)
     extern __shared__ __align__(1024) unsigned char smem[];
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem);
-    uint64_t *empty = full + kStages;
-    double *stages = reinterpret_cast<double *>(smem + 128);
-    double *rxb = stages + kStages * stage_elems;   // ALL10: [2][H][TX]
+
+    Ctx c;
+    c.TY = P.ty;
+    c.H = c.TY + 4;
+    c.nthr = TPR * c.TY;
+    c.stage_elems = round_up(W * c.H, 16);
+    c.full = reinterpret_cast<uint64_t *>(smem);
+    c.stages = reinterpret_cast<const double *>(smem + 128);
+    c.rxb = reinterpret_cast<double *>(smem + 128) + kStages * c.stage_elems;
 
     // ---- box table lookup: blockIdx.x -> (box, tile) ----
     int t = blockIdx.x;
     int b = 0;
-    while (b + 1 < P.nbox && t >= P.box[b + 1].tile_begin) ++b;
+    if constexpr (MODE == D4_LAP4) {
+        while (b + 1 < P.nbox && t >= P.box[b + 1].tile_begin) ++b;
+    }
     const BoxDesc &B = P.box[b];
     t -= B.tile_begin;
     const int bx = t % B.ntx;
     t /= B.ntx;
     const int by = t % B.nty;
     const int bz = t / B.nty;
-    const int X0 = B.ax0 + bx * TX;
-    const int Y0 = B.lo[1] + by * TY;
-    const int Z0 = B.lo[2] + bz * P.zc;
-    const int Z1 = min(Z0 + P.zc, B.hi[2]);
-    const int nplanes = Z1 - Z0 + 4;
+    c.X0 = B.ax0 + bx * TX;
+    c.Y0 = B.lo[1] + by * c.TY;
+    c.Z0 = B.lo[2] + bz * P.zc;
+    c.Z1 = min(c.Z0 + P.zc, B.hi[2]);
+    c.nplanes = c.Z1 - c.Z0 + 4;
 
-    const int tid = threadIdx.x;
-    if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], ncons / 32);
-        }
+    c.tid = threadIdx.x;
+    c.cx = c.tid % TPR;
+    c.ry = c.tid / TPR;
+    const int x = c.X0 + NP * c.cx;
+    const int y = c.Y0 + c.ry;
+    c.off_xy = (long long)x + (long long)y * B.sy;
+    Lanes<NP> L;
+    const bool yin = y < B.hi[1];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) L.m[j] = (yin && x + j >= B.lo[0] && x + j < B.hi[0]) ? 1 : 0;
+    if constexpr (NP == 2) {
+        L.full = L.m[0] & L.m[1];
+        L.only0 = L.m[0] & (L.m[1] ^ 1);
+        L.only1 = L.m[1] & (L.m[0] ^ 1);
+    }
+
+    if (c.tid == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&c.full[s], 1);
         fence_mbar_init();
+        tma_prefetch_desc(&B.tmap);
+        const uint32_t bytes = (uint32_t)(W * c.H * 8);
+        for (int i = 0; i < kStages && i < c.nplanes; ++i) {
+            mbar_arrive_expect_tx(&c.full[i], bytes);
+            tma_load_3d(const_cast<double *>(c.stages) + i * c.stage_elems, &B.tmap, B.tma0[0] + c.X0 - 2,
+                        B.tma0[1] + c.Y0 - 2, B.tma0[2] + c.Z0 - 2 + i, &c.full[i]);
+        }
     }
     __syncthreads();
 
-    if (tid >= ncons) {
-        // ---------------- producer warp: TMA plane loads ----------------
-        if (tid == ncons) {
-            tma_prefetch_desc(&B.tmap);
-            const uint32_t bytes = (uint32_t)(W * H * 8);
-            const int cx0 = B.tma0[0] + X0 - 2, cy0 = B.tma0[1] + Y0 - 2, cz0 = B.tma0[2] + Z0 - 2;
-            for (int i = 0; i < nplanes; ++i) {
-                const int s = i % kStages;
-                if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
-                mbar_arrive_expect_tx(&full[s], bytes);
-                tma_load_3d(stages + s * stage_elems, &B.tmap, cx0, cy0, cz0 + i, &full[s]);
-            }
-        }
-        return;
-    }
-
-    // ---------------- consumer threads ----------------
-    const int lane = tid & 31;
-    const int cx = tid % CPR;
-    const int ry = tid / CPR;
-    const int x = X0 + 2 * cx;
-    const int y = Y0 + ry;
-    const bool yin = y < B.hi[1];
-    const bool m0 = yin && x >= B.lo[0] && x < B.hi[0];
-    const bool m1 = yin && x + 1 >= B.lo[0] && x + 1 < B.hi[0];
-    const double k1 = P.k1, k2 = P.k2, k11 = P.k11;
-
-    double uw[5][2], sw[3][2];
-    double rxw[5][2], ryw[5][2];   // ALL10 only (dead otherwise)
+    Rings<NP> rg;
 #pragma unroll
     for (int k = 0; k < 5; ++k)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) uw[k][j] = rxw[k][j] = ryw[k][j] = 0.0;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) sw[k][0] = sw[k][1] = 0.0;
+        for (int j = 0; j < NP; ++j) rg.u[k][j] = rg.s[k][j] = rg.rx[k][j] = rg.ry[k][j] = 0.0;
 
-    for (int i = 0; i < nplanes; ++i) {
-        const int s = i % kStages;
-        const int z = Z0 - 2 + i;      // plane held by this stage
-        const int zc = z - 2;          // plane whose z terms complete now (i >= 4)
-
-        // pointwise operands of the RK stages for plane zc, issued before the wait
-        double2 pw[5];
-        if (MODE >= D4_RK1 && i >= 4) {
-            const int np = (MODE == D4_RK1) ? 1 : 5;
-#pragma unroll
-            for (int a = 0; a < 5; ++a) {
-                if (a < np) {
-                    const double *q = B.g[4 + a].at(x, y, zc);
-                    if (m0 && m1) pw[a] = load_pair(q);
-                    else {
-                        pw[a].x = m0 ? q[0] : 0.0;
-                        pw[a].y = m1 ? q[1] : 0.0;
-                    }
-                }
-            }
-        }
-
-        mbar_wait(&full[s], (i / kStages) & 1);
-        const double *pl = stages + s * stage_elems;
-        const double *row = pl + (ry + 2) * W + 2 * cx;   // element x-2 of row y
-        const double2 a0 = load_pair(row), a1 = load_pair(row + 2), a2 = load_pair(row + 4);
-        const double2 ym2 = load_pair(pl + (ry + 0) * W + 2 * cx + 2);
-        const double2 ym1 = load_pair(pl + (ry + 1) * W + 2 * cx + 2);
-        const double2 yp1 = load_pair(pl + (ry + 3) * W + 2 * cx + 2);
-        const double2 yp2 = load_pair(pl + (ry + 4) * W + 2 * cx + 2);
-
-        double rx[2] = {0.0, 0.0}, ryv[2] = {0.0, 0.0};
-        if (MODE == D4_ALL10) {
-            // x-direction unscaled first differences of this thread's halo rows
-            double *rxs = rxb + (i & 1) * H * TX;
-            for (int h = ry; h < 4; h += TY) {
-                const int hr = h < 2 ? h : TY + h;
-                const double *hrow = pl + hr * W + 2 * cx;
-                const double2 b0 = load_pair(hrow), b1 = load_pair(hrow + 2), b2 = load_pair(hrow + 4);
-                double2 r;
-                r.x = d1u(b0.x, b0.y, b1.y, b2.x);
-                r.y = d1u(b0.y, b1.x, b2.x, b2.y);
-                *reinterpret_cast<double2 *>(rxs + hr * TX + 2 * cx) = r;
-            }
-            rx[0] = d1u(a0.x, a0.y, a1.y, a2.x);
-            rx[1] = d1u(a0.y, a1.x, a2.x, a2.y);
-            ryv[0] = d1u(ym2.x, ym1.x, yp1.x, yp2.x);
-            ryv[1] = d1u(ym2.y, ym1.y, yp1.y, yp2.y);
-            *reinterpret_cast<double2 *>(rxs + (ry + 2) * TX + 2 * cx) = make_double2(rx[0], rx[1]);
-        }
-        // this warp is done reading the stage
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-
-        const double u0[2] = {a1.x, a1.y};
-        double dxx[2], dyy[2];
-        dxx[0] = d2(a0.x, a0.y, a1.x, a1.y, a2.x, k2);
-        dxx[1] = d2(a0.y, a1.x, a1.y, a2.x, a2.y, k2);
-        dyy[0] = d2(ym2.x, ym1.x, a1.x, yp1.x, yp2.x, k2);
-        dyy[1] = d2(ym2.y, ym1.y, a1.y, yp1.y, yp2.y, k2);
-
-        const bool in_plane = (z >= Z0) && (z < Z1);
-        if (MODE == D4_ALL10) {
-            named_bar(1, ncons);   // rx of all rows (incl. halo) of this plane visible
-            const double *rxs = rxb + (i & 1) * H * TX + 2 * cx;
-            const double2 r_m2 = load_pair(rxs + (ry + 0) * TX);
-            const double2 r_m1 = load_pair(rxs + (ry + 1) * TX);
-            const double2 r_p1 = load_pair(rxs + (ry + 3) * TX);
-            const double2 r_p2 = load_pair(rxs + (ry + 4) * TX);
-            if (in_plane) {
-                const double dxy0 = mul(d1u(r_m2.x, r_m1.x, r_p1.x, r_p2.x), k11);
-                const double dxy1 = mul(d1u(r_m2.y, r_m1.y, r_p1.y, r_p2.y), k11);
-                store_pair(B.g[0].at(x, y, z), mul(rx[0], k1), mul(rx[1], k1), m0, m1);
-                store_pair(B.g[1].at(x, y, z), mul(ryv[0], k1), mul(ryv[1], k1), m0, m1);
-                store_pair(B.g[3].at(x, y, z), dxx[0], dxx[1], m0, m1);
-                store_pair(B.g[4].at(x, y, z), dyy[0], dyy[1], m0, m1);
-                store_pair(B.g[6].at(x, y, z), dxy0, dxy1, m0, m1);
-            }
-        }
-
-        // ---- slide the z windows ----
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) uw[k][j] = uw[k + 1][j];
-            uw[4][j] = u0[j];
-            sw[0][j] = sw[1][j];
-            sw[1][j] = sw[2][j];
-            sw[2][j] = add(dxx[j], dyy[j]);
-            if (MODE == D4_ALL10) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    rxw[k][j] = rxw[k + 1][j];
-                    ryw[k][j] = ryw[k + 1][j];
-                }
-                rxw[4][j] = rx[j];
-                ryw[4][j] = ryv[j];
-            }
-        }
-
-        if (i < 4) continue;
-
-        // ---- plane zc: z terms complete ----
-        double dzz[2], lap[2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            dzz[j] = d2(uw[0][j], uw[1][j], uw[2][j], uw[3][j], uw[4][j], k2);
-            lap[j] = add(sw[0][j], dzz[j]);
-        }
-        if (MODE == D4_ALL10) {
-            double dz[2], dxz[2], dyz[2];
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                dz[j] = mul(d1u(uw[0][j], uw[1][j], uw[3][j], uw[4][j]), k1);
-                dxz[j] = mul(d1u(rxw[0][j], rxw[1][j], rxw[3][j], rxw[4][j]), k11);
-                dyz[j] = mul(d1u(ryw[0][j], ryw[1][j], ryw[3][j], ryw[4][j]), k11);
-            }
-            store_pair(B.g[2].at(x, y, zc), dz[0], dz[1], m0, m1);
-            store_pair(B.g[5].at(x, y, zc), dzz[0], dzz[1], m0, m1);
-            store_pair(B.g[7].at(x, y, zc), dxz[0], dxz[1], m0, m1);
-            store_pair(B.g[8].at(x, y, zc), dyz[0], dyz[1], m0, m1);
-            store_pair(B.g[9].at(x, y, zc), lap[0], lap[1], m0, m1);
-        } else if (MODE == D4_LAP4) {
-            store_pair(B.g[0].at(x, y, zc), lap[0], lap[1], m0, m1);
-        } else if (MODE == D4_RK1) {
-            // k1 = (pi0, L(phi0)); phi2 = phi0 + (dt/2) pi0; pi2 = pi0 + (dt/2) L; acc = k1
-            const double c = P.ca;
-            const double p0[2] = {pw[0].x, pw[0].y};
-            double fo[2], po[2];
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                fo[j] = add(uw[2][j], mul(c, p0[j]));
-                po[j] = add(p0[j], mul(c, lap[j]));
-            }
-            store_pair(B.g[0].at(x, y, zc), fo[0], fo[1], m0, m1);
-            store_pair(B.g[1].at(x, y, zc), po[0], po[1], m0, m1);
-            store_pair(B.g[2].at(x, y, zc), p0[0], p0[1], m0, m1);
-            store_pair(B.g[3].at(x, y, zc), lap[0], lap[1], m0, m1);
-        } else {
-            // pw: 0 pi_s, 1 phi0, 2 pi0, 3 acc_phi, 4 acc_pi
-            const double c = P.ca;
-            const double ps[2] = {pw[0].x, pw[0].y}, f0[2] = {pw[1].x, pw[1].y};
-            const double p0[2] = {pw[2].x, pw[2].y}, af[2] = {pw[3].x, pw[3].y};
-            const double ap[2] = {pw[4].x, pw[4].y};
-            double o0[2], o1[2], o2[2], o3[2];
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                if (MODE == D4_RK23) {
-                    o0[j] = add(f0[j], mul(c, ps[j]));
-                    o1[j] = add(p0[j], mul(c, lap[j]));
-                    o2[j] = add(af[j], mul(2.0, ps[j]));
-                    o3[j] = add(ap[j], mul(2.0, lap[j]));
-                } else {
-                    o0[j] = add(f0[j], mul(c, add(af[j], ps[j])));
-                    o1[j] = add(p0[j], mul(c, add(ap[j], lap[j])));
-                }
-            }
-            store_pair(B.g[0].at(x, y, zc), o0[0], o0[1], m0, m1);
-            store_pair(B.g[1].at(x, y, zc), o1[0], o1[1], m0, m1);
-            if (MODE == D4_RK23) {
-                store_pair(B.g[2].at(x, y, zc), o2[0], o2[1], m0, m1);
-                store_pair(B.g[3].at(x, y, zc), o3[0], o3[1], m0, m1);
-            }
-        }
+    for (int i = 0;; i += 5) {
+        if (plane_step<MODE, TX, NP, 0>(i + 0, c, P, B, L, rg)) break;
+        if (plane_step<MODE, TX, NP, 1>(i + 1, c, P, B, L, rg)) break;
+        if (plane_step<MODE, TX, NP, 2>(i + 2, c, P, B, L, rg)) break;
+        if (plane_step<MODE, TX, NP, 3>(i + 3, c, P, B, L, rg)) break;
+        if (plane_step<MODE, TX, NP, 4>(i + 4, c, P, B, L, rg)) break;
     }
 }
 
-template <int MODE, int TX>
+size_t smem_bytes(int mode, int tx, int ty) {
+    const int H = ty + 4;
+    size_t smem = 128 + (size_t)kStages * round_up((tx + 4) * H, 16) * 8;
+    if (mode == D4_ALL10) smem += (size_t)2 * H * tx * 8;
+    return smem;
+}
+
+template <int MODE, int TX, int NP>
 int launch_mode_tx(const D4Params &P, int nblocks, cudaStream_t st) {
-    const int ncons = (TX / 2) * P.ty;
-    const int threads = ncons + 32;
-    const int H = P.ty + 4;
-    size_t smem = 128 + (size_t)kStages * round_up((TX + 4) * H, 16) * 8;
-    if (MODE == D4_ALL10) smem += (size_t)2 * H * TX * 8;
-    auto fn = d4_kernel<MODE, TX>;
+    const int threads = (TX / NP) * P.ty;
+    const size_t smem = smem_bytes(MODE, TX, P.ty);
+    auto fn = d4_kernel<MODE, TX, NP>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(d4)");
     fn<<<nblocks, threads, smem, st>>>(P);
     return check_cuda(cudaGetLastError(), "d4_kernel launch");
 }
 
-template <int MODE>
+template <int MODE, int NP>
 int launch_mode(const D4Params &P, int tx, int nblocks, cudaStream_t st) {
     switch (tx) {
-        case 32: return launch_mode_tx<MODE, 32>(P, nblocks, st);
-        case 64: return launch_mode_tx<MODE, 64>(P, nblocks, st);
-        case 128: return launch_mode_tx<MODE, 128>(P, nblocks, st);
+        case 32: return launch_mode_tx<MODE, 32, NP>(P, nblocks, st);
+        case 64: return launch_mode_tx<MODE, 64, NP>(P, nblocks, st);
+        case 128: return launch_mode_tx<MODE, 128, NP>(P, nblocks, st);
         default: return fail(SB_USAGE, "tile_x must be 32, 64 or 128");
     }
 }
+
+template <int MODE>
+int launch_np(const D4Params &P, int tx, int np, int nblocks, cudaStream_t st) {
+    return np == 1 ? launch_mode<MODE, 1>(P, tx, nblocks, st) : launch_mode<MODE, 2>(P, tx, nblocks, st);
+}
+
+bool same_strides(const sb_array &a, const sb_array &b) { return a.sy == b.sy && a.sz == b.sz; }
 
 }  // namespace
 
 int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, double ca, double cb,
               const sb_launch &p, cudaStream_t st) {
+    (void)cb;
     if (njobs < 1 || njobs > SB_MAX_BOXES) return fail(SB_RESOURCE, "box count outside 1..SB_MAX_BOXES");
     const int TX = p.tile_x, TY = p.tile_y, ZC = p.z_chunk;
+    const int NP = (p.flags & SB_LAUNCH_SCALAR) ? 1 : 2;
     if (TX != 32 && TX != 64 && TX != 128) return fail(SB_USAGE, "tile_x must be 32, 64 or 128");
     if (TY < 1 || ZC < 1) return fail(SB_USAGE, "tile_y and z_chunk must be positive");
-    const int ncons = (TX / 2) * TY;
-    if (ncons % 32 != 0 || ncons > max_consumers(mode))
-        return fail(SB_USAGE, "(tile_x/2)*tile_y must be a multiple of 32 and <= 256 (d4_all) / 512 (others)");
+    const int threads = (TX / NP) * TY;
+    if (threads % 32 != 0 || threads > max_threads(mode, NP))
+        return fail(SB_USAGE, "threads per CTA ((tile_x/points per thread)*tile_y) must be a multiple of 32 and "
+                              "within the mode's limit (256 for paired d4_all / RK stages, else 512)");
     if (TY + 4 > 256) return fail(SB_USAGE, "tile_y + 4 exceeds the TMA box limit of 256");
-    const int H = TY + 4;
-    size_t smem = 128 + (size_t)kStages * round_up((TX + 4) * H, 16) * 8;
-    if (mode == D4_ALL10) smem += (size_t)2 * H * TX * 8;
-    if (smem > 227 * 1024) return fail(SB_RESOURCE, "tile needs more than 227 KB of shared memory");
+    if (smem_bytes(mode, TX, TY) > 227 * 1024) return fail(SB_RESOURCE, "tile needs more than 227 KB of shared memory");
+    const int nused = mode == D4_ALL10 ? 10 : mode == D4_LAP4 ? 1 : mode == D4_RK1 ? 5 : 9;
 
     D4Params P;
     memset(&P, 0, sizeof(P));
@@ -349,8 +447,7 @@ int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, 
     P.k2 = k.k2;
     P.k11 = k.k11;
     P.ca = ca;
-    P.cb = cb;
-    int total = 0;
+    long long total = 0;
     int nbox = 0;
     for (int j = 0; j < njobs; ++j) {
         const D4Job &J = jobs[j];
@@ -358,10 +455,15 @@ int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, 
         bool empty = false;
         for (int d = 0; d < 3; ++d) empty |= sp.hi[d] <= sp.lo[d];
         if (empty) continue;
+        for (int a = 1; a < nused; ++a)
+            if (!same_strides(J.g[a], J.g[0]))
+                return fail(SB_USAGE, "all output / pointwise grids of one box must share row and plane strides");
         BoxDesc &D = P.box[nbox];
         int rc = make_tmap(&D.tmap, J.src, TX + 4, TY + 4, 1);
         if (rc) return rc;
-        for (int a = 0; a < 10; ++a) D.g[a] = grid_of(J.g[a]);
+        for (int a = 0; a < 10; ++a) D.g[a] = J.g[a].origin;
+        D.sy = J.g[0].sy;
+        D.sz = J.g[0].sz;
         D.tma0[0] = J.src.xpad;
         D.tma0[1] = J.src.ghost;
         D.tma0[2] = J.src.ghost;
@@ -372,21 +474,22 @@ int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, 
         D.ax0 = (sp.lo[0] >= 0 ? sp.lo[0] / TX : -((-sp.lo[0] + TX - 1) / TX)) * TX;
         D.ntx = (sp.hi[0] - D.ax0 + TX - 1) / TX;
         D.nty = (sp.hi[1] - sp.lo[1] + TY - 1) / TY;
-        D.ntz = (sp.hi[2] - sp.lo[2] + ZC - 1) / ZC;
-        D.tile_begin = total;
-        const long long nt = (long long)D.ntx * D.nty * D.ntz;
-        if (total + nt > 0x7fffffffLL) return fail(SB_RESOURCE, "too many tiles for one launch");
-        total += (int)nt;
+        const int ntz = (sp.hi[2] - sp.lo[2] + ZC - 1) / ZC;
+        D.tile_begin = (int)total;
+        total += (long long)D.ntx * D.nty * ntz;
+        if (total > 0x7fffffffLL) return fail(SB_RESOURCE, "too many tiles for one launch");
         ++nbox;
     }
     if (nbox == 0) return SB_OK;
+    if (nbox > 1 && mode != D4_LAP4) return fail(SB_USAGE, "only the Laplacian sweeps several boxes per launch");
     P.nbox = nbox;
+    const int nb = (int)total;
     switch (mode) {
-        case D4_ALL10: return launch_mode<D4_ALL10>(P, TX, total, st);
-        case D4_LAP4: return launch_mode<D4_LAP4>(P, TX, total, st);
-        case D4_RK1: return launch_mode<D4_RK1>(P, TX, total, st);
-        case D4_RK23: return launch_mode<D4_RK23>(P, TX, total, st);
-        case D4_RK4: return launch_mode<D4_RK4>(P, TX, total, st);
+        case D4_ALL10: return launch_np<D4_ALL10>(P, TX, NP, nb, st);
+        case D4_LAP4: return launch_np<D4_LAP4>(P, TX, NP, nb, st);
+        case D4_RK1: return launch_np<D4_RK1>(P, TX, NP, nb, st);
+        case D4_RK23: return launch_np<D4_RK23>(P, TX, NP, nb, st);
+        case D4_RK4: return launch_np<D4_RK4>(P, TX, NP, nb, st);
         default: return fail(SB_USAGE, "unknown d4 mode");
     }
 }

@@ -27,9 +27,12 @@ from .inputs import N_TERMS, N_VARS, D4Constants, PolyTable, WaveConstants
 from .traverse import IndexSpace
 from .tuner import LaunchParams, LaunchSpace
 
-D4_ALL_SPACE = LaunchSpace(kind="d4_all", max_threads=256, rx_buffer=True)
-D4_SPACE = LaunchSpace(kind="d4", max_threads=512)
-LAP7_SPACE = LaunchSpace(kind="lap7", max_threads=256, radius=1, stages=0, tile_xs=(64,), tile_ys=(1, 2, 4, 8))
+# launch spaces: thread caps mirror max_threads() in csrc/d4.cu (register budgets)
+D4_ALL_SPACE = LaunchSpace(kind="d4_all", max_threads_pair=256, max_threads_scalar=512, rx_buffer=True)
+D4_SPACE = LaunchSpace(kind="lap4", max_threads_pair=512, max_threads_scalar=512)
+RK4_SPACE = LaunchSpace(kind="rk4", max_threads_pair=256, max_threads_scalar=512)
+LAP7_SPACE = LaunchSpace(kind="lap7", max_threads_pair=256, radius=1, stages=0, tile_xs=(64,),
+                         tile_ys=(1, 2, 4, 8), points=(2,))
 
 
 def _local(space: IndexSpace, grid: DeviceGrid) -> _lib.sb_space:
@@ -83,7 +86,7 @@ class Laplacian7(DeviceKernel):
 
     def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
         _lib.call("sb_lap7", self.dst.abi(), self.src.abi(), _local(space, self.src), self.c0, self.c1,
-                  _lib.launch(params.tile_x, params.tile_y, params.z_chunk), stream_ptr(stream))
+                  _lib.launch_of(params), stream_ptr(stream))
 
 
 class FourthOrderAll(DeviceKernel):
@@ -106,7 +109,7 @@ class FourthOrderAll(DeviceKernel):
 
     def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
         _lib.call("sb_d4_all", self._out_abi, self.src.abi(), _local(space, self.src), _lib.d4_constants(self.k),
-                  _lib.launch(params.tile_x, params.tile_y, params.z_chunk), stream_ptr(stream))
+                  _lib.launch_of(params), stream_ptr(stream))
 
 
 class Laplacian4(DeviceKernel):
@@ -127,7 +130,7 @@ class Laplacian4(DeviceKernel):
     def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
         job = _lib.sb_box_job(self.dst.abi(), self.src.abi(), _local(space, self.src))
         _lib.call("sb_lap4_boxes", C.byref(job), 1, _lib.d4_constants(self.k),
-                  _lib.launch(params.tile_x, params.tile_y, params.z_chunk), stream_ptr(stream))
+                  _lib.launch_of(params), stream_ptr(stream))
 
 
 class LevelLaplacian4(DeviceKernel):
@@ -171,7 +174,7 @@ class LevelLaplacian4(DeviceKernel):
             chunk = jobs[i:i + _lib.SB_MAX_BOXES]
             arr = (_lib.sb_box_job * len(chunk))(*chunk)
             _lib.call("sb_lap4_boxes", arr, len(chunk), _lib.d4_constants(self.k),
-                      _lib.launch(params.tile_x, params.tile_y, params.z_chunk), stream_ptr(stream))
+                      _lib.launch_of(params), stream_ptr(stream))
 
     def launch(self, space: IndexSpace | None, params: LaunchParams, stream=None) -> None:
         self._run(self._jobs(None if space is None else space), params, stream)
@@ -215,7 +218,7 @@ class WaveRK4:
                                self.acc_pi.abi(), phi_out.abi(), pi_out.abi())
         n = self.n
         _lib.call("sb_rk4_stage", s, C.byref(f), _lib.space((0, 0, 0), (n, n, n)), self._consts(),
-                  _lib.launch(params.tile_x, params.tile_y, params.z_chunk), stream_ptr(stream))
+                  _lib.launch_of(params), stream_ptr(stream))
 
     def step(self, params: LaunchParams | None = None, stream=None) -> tuple[DeviceGrid, DeviceGrid]:
         """One RK4 step from (phi0, pi0); returns the grids holding the new state
@@ -238,7 +241,7 @@ class Rhs24(DeviceKernel):
     """K6 — config-5 fused 24-variable right-hand side."""
 
     site_id = "rhs24"
-    space_kind = LaunchSpace(kind="rhs24", max_threads=512, tile_xs=(32, 64, 128))
+    space_kind = LaunchSpace(kind="rhs24", max_threads_pair=512, points=(2,))
     default_params = LaunchParams(64, 8, 32)   # fixed 8x4x2 point blocks; params unused
 
     def __init__(self, ins: list[DeviceGrid], outs: list[DeviceGrid], k: D4Constants, poly: PolyTable):
@@ -260,4 +263,4 @@ class Rhs24(DeviceKernel):
     def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
         poly = _lib.sb_poly(self._coef.ctypes.data, self._p.ctypes.data, self._q.ctypes.data)
         _lib.call("sb_rhs24", self._in, self._out, _local(space, self.ins[0]), _lib.d4_constants(self.k), poly,
-                  _lib.launch(params.tile_x, params.tile_y, params.z_chunk), stream_ptr(stream))
+                  _lib.launch_of(params), stream_ptr(stream))

@@ -130,14 +130,16 @@ class ExecParams:
 
 @dataclass(frozen=True)
 class LaunchParams:
-    """One point of the device space: CTA tile (x, y) and z planes per CTA."""
+    """One point of the device space: CTA tile (x, y), z planes per CTA, and
+    x points per thread (2 = one 16-byte pair, the device's SIMD width W)."""
 
     tile_x: int
     tile_y: int
     z_chunk: int
+    points_per_thread: int = 2
 
     def flat(self) -> str:
-        return f"{self.tile_x}x{self.tile_y}/z{self.z_chunk}"
+        return f"{self.tile_x}x{self.tile_y}/z{self.z_chunk}/p{self.points_per_thread}"
 
 
 class ParamSpace(Protocol):
@@ -329,13 +331,15 @@ def _valid_unique(space, p, cand, setup, topo) -> list:
 class LaunchSpace:
     """CTA tile x/y and z chunk of a z-streaming sm_100a stencil kernel.
 
-    ``max_threads`` bounds (tile_x/2)*tile_y (consumer threads; one producer
-    warp is added), ``smem_bytes(tile_x, tile_y)`` the shared memory a CTA
-    needs, ``pair_threads`` whether a thread owns two x points (so
-    (tile_x/2)*tile_y must be a multiple of 32)."""
+    Threads per CTA are (tile_x / points_per_thread) * tile_y, a multiple of 32
+    bounded by ``max_threads_pair`` / ``max_threads_scalar`` (the register
+    budget of the kernel variant); ``smem_bytes(tile_x, tile_y)`` is the
+    shared memory a CTA needs."""
 
     kind: str = "d4"
-    max_threads: int = 512
+    max_threads_pair: int = 512
+    max_threads_scalar: int = 512
+    points: tuple[int, ...] = (2, 1)
     radius: int = 2
     rx_buffer: bool = False     # d4_all keeps a double-buffered rx plane in smem
     stages: int = 4
@@ -360,9 +364,12 @@ class LaunchSpace:
             raise UsageError(f"tile_x {p.tile_x} not in {self.tile_xs}")
         if p.tile_y < 1 or p.z_chunk < 1:
             raise UsageError("tile_y and z_chunk must be positive")
-        threads = (p.tile_x // 2) * p.tile_y
-        if threads % 32 or threads > self.max_threads:
-            raise UsageError(f"(tile_x/2)*tile_y = {threads} not a multiple of 32 in 32..{self.max_threads}")
+        if p.points_per_thread not in self.points:
+            raise UsageError(f"points_per_thread {p.points_per_thread} not in {self.points}")
+        cap = self.max_threads_pair if p.points_per_thread == 2 else self.max_threads_scalar
+        threads = (p.tile_x // p.points_per_thread) * p.tile_y
+        if threads % 32 or threads > cap:
+            raise UsageError(f"{threads} threads per CTA not a multiple of 32 in 32..{cap}")
         if p.tile_y + 2 * self.radius > 256:
             raise UsageError("tile_y exceeds the TMA box limit")
         if self.smem_bytes(p.tile_x, p.tile_y) > topo.smem_per_block:
@@ -374,37 +381,41 @@ class LaunchSpace:
     def enumerate(self, setup: LoopSetup, topo: TopologyConfig) -> list[LaunchParams]:
         nz = setup.extents[2] if setup.dim >= 3 else 1
         out = []
-        for tx in self.tile_xs:
-            for ty in self.tile_ys:
-                for zc in self._z_values(nz):
-                    p = LaunchParams(tx, ty, zc)
-                    try:
-                        self.check(p, setup, topo)
-                    except UsageError:
-                        continue
-                    out.append(p)
+        for pp in self.points:
+            for tx in self.tile_xs:
+                for ty in self.tile_ys:
+                    for zc in self._z_values(nz):
+                        p = LaunchParams(tx, ty, zc, pp)
+                        try:
+                            self.check(p, setup, topo)
+                        except UsageError:
+                            continue
+                        out.append(p)
         return out
 
     def random(self, setup: LoopSetup, topo: TopologyConfig, rng: random.Random) -> LaunchParams:
         return rng.choice(self.enumerate(setup, topo))
 
     def initial(self, setup: LoopSetup, topo: TopologyConfig) -> LaunchParams:
-        """64-wide tiles (one warp = one 512-byte row of doubles); the largest
-        tile_y allowed; z chunk chosen so the grid covers the SMs >= 4 times."""
+        """64-wide tiles (a row of doubles is 512 bytes), the first listed
+        points-per-thread, tile_y up to 8, z chunk chosen so the grid covers
+        the SMs >= 4 times."""
         valid = self.enumerate(setup, topo)
         if not valid:
             raise UsageError(f"no valid launch parameters for {setup}")
         nx, ny = setup.extents[0], setup.extents[1] if setup.dim >= 2 else 1
         nz = setup.extents[2] if setup.dim >= 3 else 1
-        tx = 64 if any(p.tile_x == 64 for p in valid) else valid[0].tile_x
-        ty = max(p.tile_y for p in valid if p.tile_x == tx and p.tile_y <= 8)
+        pp = next((q for q in self.points if any(p.points_per_thread == q for p in valid)), valid[0].points_per_thread)
+        mine = [p for p in valid if p.points_per_thread == pp]
+        tx = 64 if any(p.tile_x == 64 for p in mine) else mine[0].tile_x
+        ty = max((p.tile_y for p in mine if p.tile_x == tx and p.tile_y <= 8), default=mine[0].tile_y)
         cols = -(-nx // tx) * -(-ny // ty)
         zc = nz
-        for cand in sorted({p.z_chunk for p in valid}, reverse=True):
+        for cand in sorted({p.z_chunk for p in mine}, reverse=True):
             zc = cand
             if cols * -(-nz // cand) >= 4 * topo.sm_count:
                 break
-        p = LaunchParams(tx, ty, zc)
+        p = LaunchParams(tx, ty, zc, pp)
         self.check(p, setup, topo)
         return p
 
@@ -418,6 +429,11 @@ class LaunchSpace:
                 cand.append(replace(p, **{f: v // 2}))
         if p.z_chunk != nz:
             cand.append(replace(p, z_chunk=nz))
+        for q in self.points:
+            if q != p.points_per_thread:
+                # same threads per CTA: trade tile_y against points per thread
+                cand.append(replace(p, points_per_thread=q))
+                cand.append(replace(p, points_per_thread=q, tile_y=max(1, p.tile_y * p.points_per_thread // q)))
         return _valid_unique(self, p, cand, setup, topo)
 
 
@@ -584,7 +600,8 @@ class TuningCache:
     def put(self, setup: LoopSetup, space, params, seconds: float) -> None:
         if not isinstance(params, LaunchParams):
             return
-        self._d[self._key(setup)] = {"params": [params.tile_x, params.tile_y, params.z_chunk], "seconds": seconds}
+        self._d[self._key(setup)] = {"params": [params.tile_x, params.tile_y, params.z_chunk,
+                                                params.points_per_thread], "seconds": seconds}
         tmp = self.path.with_suffix(".tmp")
         tmp.write_text(json.dumps(self._d, indent=1, sort_keys=True))
         os.replace(tmp, self.path)
