@@ -205,8 +205,31 @@ def run_ours(args) -> None:
         dist.barrier()
 
     prob = C2FourthOrder().setup()
-    params = LaunchParams(*args.params) if args.params else prob.kernel.default_params
     stream = torch.cuda.current_stream()
+
+    # run-time auto-tuning of the launch shape (the reference's LoopControl
+    # tuner state machine over the device launch space), during warm-up
+    tune_info = None
+    if args.params:
+        params = LaunchParams(*args.params)
+    elif args.tune > 0:
+        from paper_1308_1343_b200.traverse import run_loop
+        from paper_1308_1343_b200.tuner import LoopSetup, TopologyConfig, Tuner
+        kern = prob.kernel
+        setup = LoopSetup(kern.site_id, kern.full_space().extents)
+        tuner = Tuner(TopologyConfig())
+        tuner.prime(setup, kern.launch_space(), kern.default_params)
+        for _ in range(args.tune):
+            run_loop(setup, prob.space, kern, tuner)
+        params, best_s = tuner.best(setup)
+        if dist:   # every rank runs rank 0's choice
+            obj = [params]
+            dist.broadcast_object_list(obj, src=0)
+            params = obj[0]
+        tune_info = {"executions": args.tune, "best": params.flat(), "best_median_ms": best_s * 1e3,
+                     "start": kern.default_params.flat(), "distinct_tried": len({r["params"] for r in tuner.log})}
+    else:
+        params = prob.kernel.default_params
 
     def barrier():
         if dist:
@@ -276,7 +299,8 @@ def run_ours(args) -> None:
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded host generator, BASELINE.json config 2 shapes)",
         "config": dict(WORKLOAD, parallelism=f"box-per-rank x{world}",
-                       launch={"tile_x": params.tile_x, "tile_y": params.tile_y, "z_chunk": params.z_chunk}),
+                       launch={"tile_x": params.tile_x, "tile_y": params.tile_y, "z_chunk": params.z_chunk,
+                               "points_per_thread": params.points_per_thread}, tuning=tune_info),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks else "fallback",
                      "algorithmic_bytes_per_launch": prob.canonical_bytes, "kernel_ms_mean": kernel_ms,
@@ -300,7 +324,9 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--params", type=int, nargs=3, default=None, metavar=("TILE_X", "TILE_Y", "Z_CHUNK"))
+    ap.add_argument("--params", type=int, nargs=4, default=None,
+                    metavar=("TILE_X", "TILE_Y", "Z_CHUNK", "POINTS_PER_THREAD"))
+    ap.add_argument("--tune", type=int, default=40, help="tuner executions during warm-up (0 = kernel default)")
     ap.add_argument("--e2e-steps", dest="e2e_steps", type=int, default=10)
     ap.add_argument("--ref-seconds", dest="ref_seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", dest="no_cpu", action="store_true")

@@ -94,7 +94,8 @@ class FourthOrderAll(DeviceKernel):
 
     site_id = "d4_all"
     space_kind = D4_ALL_SPACE
-    default_params = LaunchParams(64, 4, 32)
+    # best of the full launch-space sweep at 256^3 on B200 (profiles/r01/v2_sweep_c2.jsonl)
+    default_params = LaunchParams(32, 4, 4, 2)
 
     def __init__(self, outs: list[DeviceGrid], src: DeviceGrid, k: D4Constants):
         if len(outs) != _lib.SB_N_D4_OUT:
@@ -117,7 +118,7 @@ class Laplacian4(DeviceKernel):
 
     site_id = "lap4"
     space_kind = D4_SPACE
-    default_params = LaunchParams(64, 8, 32)
+    default_params = LaunchParams(32, 4, 128, 2)
 
     def __init__(self, dst: DeviceGrid, src: DeviceGrid, k: D4Constants):
         if src.ghost < 2:
@@ -141,7 +142,8 @@ class LevelLaplacian4(DeviceKernel):
 
     site_id = "lap4_level"
     space_kind = D4_SPACE
-    default_params = LaunchParams(64, 8, 32)
+    # best of the sweep on the config-4 level (profiles/r01/v2_sweep_c4.jsonl)
+    default_params = LaunchParams(32, 4, 128, 2)
 
     def __init__(self, dsts: list[DeviceGrid], srcs: list[DeviceGrid], k: D4Constants):
         if len(dsts) != len(srcs) or not srcs:
@@ -206,7 +208,8 @@ class WaveRK4:
         self.phi0, self.pi0 = mk(), mk()
         self.phi_a, self.pi_a, self.phi_b, self.pi_b = mk(), mk(), mk(), mk()
         self.acc_phi, self.acc_pi = mk(), mk()
-        self.params = LaunchParams(64, 8, 32)
+        # best of the sweep at 384^3 (profiles/r01/v2_sweep_c3.jsonl)
+        self.params = LaunchParams(128, 2, 256, 1)
 
     def _consts(self) -> _lib.sb_rk4_constants:
         return _lib.sb_rk4_constants(_lib.d4_constants(self.c.lap), self.c.half_dt, self.c.dt, self.c.dt6)

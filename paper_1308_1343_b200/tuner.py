@@ -486,6 +486,15 @@ class Tuner:
             self._states[setup] = st
         return st
 
+    def prime(self, setup: LoopSetup, space, start) -> None:
+        """Start a not-yet-seen setup's climb at `start` (e.g. a kernel's
+        measured default) instead of the space's heuristic."""
+        if setup in self._states:
+            return
+        space.check(start, setup, self.topo)
+        rng = random.Random(f"{self.topo.rng_seed}:{setup.site_id}:{setup.extents}")
+        self._states[setup] = _State(rng=rng, space=space, current=start)
+
     def space_of(self, setup: LoopSetup):
         return self._states[setup].space if setup in self._states else None
 

@@ -1,0 +1,168 @@
+"""Tuner state machine and the device launch space, driven by a fake timer
+(the reference's SyntheticSurface pattern, synthetic.py:25-58)."""
+import math
+import random
+
+import pytest
+
+from paper_1308_1343_b200.errors import UsageError
+from paper_1308_1343_b200.kernels import D4_ALL_SPACE, D4_SPACE, LAP7_SPACE, RK4_SPACE
+from paper_1308_1343_b200.tuner import (
+    ExecParams, LaunchParams, LaunchSpace, LoopSetup, PlanSpace, TopologyConfig, Tuner, TuningCache,
+)
+
+
+def test_topology_file(tmp_path):
+    f = tmp_path / "topology.cfg"
+    f.write_text("# comment\ncache_size_bytes = 1048576\nn_coarse_threads=4  # four\np_restart = 0.1\nsm_count = 148\n")
+    t = TopologyConfig.from_file(f)
+    assert (t.cache_size_bytes, t.n_coarse_threads, t.p_restart, t.sm_count) == (1048576, 4, 0.1, 148)
+    f.write_text("bogus = 1\n")
+    with pytest.raises(UsageError):
+        TopologyConfig.from_file(f)
+    f.write_text("no equals sign\n")
+    with pytest.raises(UsageError):
+        TopologyConfig.from_file(f)
+
+
+def test_plan_space_initial_and_neighbors_valid():
+    topo = TopologyConfig(n_coarse_threads=4, n_fine_threads=2, lane_width=4)
+    space = PlanSpace()
+    for ext in [(64, 64, 64), (130, 7, 3), (5,), (16, 16)]:
+        setup = LoopSetup("s", ext, "vector", 4, 2)
+        p = space.initial(setup, topo)
+        space.check(p, setup, topo)
+        for q in space.neighbors(p, setup, topo):
+            space.check(q, setup, topo)
+            assert q != p
+
+
+@pytest.mark.parametrize("space", [D4_ALL_SPACE, D4_SPACE, RK4_SPACE, LAP7_SPACE])
+def test_launch_space_invariants(space):
+    topo = TopologyConfig()
+    setup = LoopSetup("k", (256, 256, 256))
+    valid = space.enumerate(setup, topo)
+    assert valid
+    for p in valid:
+        threads = (p.tile_x // p.points_per_thread) * p.tile_y
+        assert threads % 32 == 0
+        assert space.smem_bytes(p.tile_x, p.tile_y) <= topo.smem_per_block
+    p0 = space.initial(setup, topo)
+    space.check(p0, setup, topo)
+    for q in space.neighbors(p0, setup, topo):
+        space.check(q, setup, topo)
+    with pytest.raises(UsageError):
+        space.check(LaunchParams(48, 4, 8), setup, topo)
+
+
+def test_d4_all_space_matches_kernel_register_budget():
+    topo = TopologyConfig()
+    setup = LoopSetup("k", (256, 256, 256))
+    with pytest.raises(UsageError):
+        D4_ALL_SPACE.check(LaunchParams(64, 16, 8, 2), setup, topo)   # 512 paired threads
+    D4_ALL_SPACE.check(LaunchParams(64, 8, 8, 1), setup, topo)         # 512 scalar threads
+
+
+class FakeSurface:
+    """Deterministic cost per launch shape with a unique optimum plus noise."""
+
+    def __init__(self, space, setup, topo, seed):
+        rng = random.Random(seed)
+        self.cost = {p: 1.0 + rng.random() * 3 for p in space.enumerate(setup, topo)}
+        self.best = min(self.cost, key=self.cost.get)
+        self.cost[self.best] = 0.5
+        self.rng = rng
+
+    def __call__(self, p):
+        return self.cost[p] * (1 + 0.02 * self.rng.random())
+
+
+def test_state_machine_converges_and_is_deterministic():
+    topo = TopologyConfig(p_restart=0.2)
+    setup = LoopSetup("fake", (256, 256, 256))
+    space = D4_SPACE
+    runs = []
+    for _ in range(2):
+        surf = FakeSurface(space, setup, topo, 7)
+        tuner = Tuner(topo, space=space)
+        seq = []
+        for _ in range(400):
+            p = tuner.next_params(setup)
+            seq.append(p)
+            tuner.record_timing(setup, p, surf(p))
+        runs.append((seq, tuner.best(setup), surf.cost[seq[0]], sorted(surf.cost.values())))
+    assert runs[0][0] == runs[1][0]
+    (best, t), start_cost, costs = runs[0][1], runs[0][2], runs[0][3]
+    assert math.isfinite(t) and best is not None
+    assert t <= start_cost * 1.02                      # never worse than where it started
+    assert t <= costs[len(costs) // 10] * 1.02         # and within the best decile of the space
+
+
+def test_warmup_median_and_abort():
+    topo = TopologyConfig(p_restart=1.0, abort_factor=1.5)
+    setup = LoopSetup("fake2", (64, 64, 64))
+    tuner = Tuner(topo, space=D4_SPACE)
+    p = tuner.next_params(setup)
+    tuner.record_timing(setup, p, 100.0)          # warm-up: discarded
+    assert tuner.best(setup) == (None, float("inf"))
+    tuner.record_timing(setup, p, 1.0)
+    assert tuner.best(setup) == (p, 1.0)
+    # an excursion sample much worse than best is abandoned immediately
+    seen_excursion = False
+    for _ in range(200):
+        q = tuner.next_params(setup)
+        if tuner.phase(setup) == "excursion":
+            seen_excursion = True
+            tuner.record_timing(setup, q, 10.0)
+            r = tuner.next_params(setup)
+            assert r == tuner.best(setup)[0]
+            tuner.record_timing(setup, r, 1.0)
+            break
+        tuner.record_timing(setup, q, 1.0 if q == p else 2.0)
+    assert seen_excursion
+    with pytest.raises(UsageError):
+        tuner.record_timing(setup, p, float("nan"))
+
+
+def test_setups_are_isolated_and_log_schema(tmp_path):
+    tuner = Tuner(TopologyConfig(), space=D4_SPACE)
+    a, b = LoopSetup("a", (64, 64, 64)), LoopSetup("b", (32, 32, 32))
+    for s in (a, b, a, b, a):
+        p = tuner.next_params(s)
+        tuner.record_timing(s, p, 1.0)
+    assert tuner.best(a)[0] is not None and tuner.best(b)[0] is not None
+    out = tmp_path / "log.csv"
+    tuner.write_log(out)
+    lines = out.read_text().splitlines()
+    assert lines[0] == "setup_id,params,elapsed_ns,phase,is_best"
+    assert len(lines) == 6 and all(len(l.split(",")) == 5 for l in lines)
+    assert {l.split(",")[3] for l in lines[1:]} <= {"warmup", "initial", "climbing", "excursion"}
+
+
+def test_prime_and_tuning_cache(tmp_path):
+    setup = LoopSetup("d4_all", (256, 256, 256))
+    start = LaunchParams(32, 4, 4, 2)
+    tuner = Tuner(TopologyConfig())
+    tuner.prime(setup, D4_ALL_SPACE, start)
+    assert tuner.next_params(setup) == start
+    cache = TuningCache(tmp_path / "cache.json")
+    t2 = Tuner(TopologyConfig(), space=D4_ALL_SPACE, cache=cache)
+    p = t2.next_params(setup)
+    t2.record_timing(setup, p, 1.0)
+    t2.record_timing(setup, p, 0.5)
+    again = TuningCache(tmp_path / "cache.json")
+    assert again.get(setup, D4_ALL_SPACE) == p
+    t3 = Tuner(TopologyConfig(), space=D4_ALL_SPACE, cache=again)
+    assert t3.next_params(setup) == p
+
+
+def test_exec_params_flat_matches_reference_format():
+    assert ExecParams((2, 1), (8, 4), (1, 2), 4).flat() == "2x1/8x4/1x2/w4"
+    assert LaunchParams(32, 4, 8, 2).flat() == "32x4/z8/p2"
+
+
+def test_launch_space_custom():
+    sp = LaunchSpace(kind="x", tile_xs=(64,), tile_ys=(4,), points=(2,))
+    setup = LoopSetup("k", (128, 128, 16))
+    vals = sp.enumerate(setup, TopologyConfig())
+    assert {p.z_chunk for p in vals} == {4, 8, 16}
