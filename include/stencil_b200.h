@@ -90,6 +90,11 @@ typedef struct sb_launch {
 
 /* sb_launch.flags: one x point per thread instead of a 16-byte pair. */
 #define SB_LAUNCH_SCALAR 1
+/* sb_launch.flags (sb_rk4_stage): also write every ghost point of phi_out
+ * that is the periodic image of an updated interior point, so the next
+ * stage needs no separate sb_ghost_periodic (the space must be the whole
+ * interior). */
+#define SB_LAUNCH_PERIODIC_GHOSTS 2
 
 /* 4th-order constants: k1 = 1/(12h), k2 = 1/(12h^2), k11 = 1/(144h^2). */
 typedef struct sb_d4_constants {

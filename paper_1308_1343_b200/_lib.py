@@ -134,16 +134,18 @@ def space(lo, hi) -> sb_space:
 
 
 SB_LAUNCH_SCALAR = 1
+SB_LAUNCH_PERIODIC_GHOSTS = 2
 
 
-def launch(tile_x: int, tile_y: int, z_chunk: int, points_per_thread: int = 2) -> sb_launch:
-    flags = SB_LAUNCH_SCALAR if points_per_thread == 1 else 0
-    return sb_launch(int(tile_x), int(tile_y), int(z_chunk), flags)
+def launch(tile_x: int, tile_y: int, z_chunk: int, points_per_thread: int = 2, flags: int = 0) -> sb_launch:
+    if points_per_thread == 1:
+        flags |= SB_LAUNCH_SCALAR
+    return sb_launch(int(tile_x), int(tile_y), int(z_chunk), int(flags))
 
 
-def launch_of(p) -> sb_launch:
-    """sb_launch of a tuner.LaunchParams."""
-    return launch(p.tile_x, p.tile_y, p.z_chunk, getattr(p, "points_per_thread", 2))
+def launch_of(p, flags: int = 0) -> sb_launch:
+    """sb_launch of a tuner.LaunchParams (plus extra SB_LAUNCH_* flags)."""
+    return launch(p.tile_x, p.tile_y, p.z_chunk, getattr(p, "points_per_thread", 2), flags)
 
 
 def d4_constants(k) -> sb_d4_constants:

@@ -104,8 +104,9 @@ class C3WaveRK4:
 
     name = "c3_wave_rk4"
 
-    def __init__(self, n: int = 384, seed: int | None = None, g: int = 2):
+    def __init__(self, n: int = 384, seed: int | None = None, g: int = 2, fused_ghosts: bool = True):
         self.n, self.g = n, g
+        self.fused_ghosts = fused_ghosts
         self.host_phi, self.host_pi = inputs.c3_fields(n, g, seed)
         self.c = inputs.WaveConstants.for_grid(n)
         self.updates = n ** 3
@@ -114,7 +115,7 @@ class C3WaveRK4:
         self.ghost_fill_bytes = 8 * 4 * 2 * (_vol((n,) * 3, g) - n ** 3)
 
     def setup(self, device=None):
-        self.rk = WaveRK4(self.n, self.g, self.c, device)
+        self.rk = WaveRK4(self.n, self.g, self.c, device, fused_ghosts=self.fused_ghosts)
         self.reset()
         return self
 
@@ -127,6 +128,9 @@ class C3WaveRK4:
 
     def outputs(self) -> list[np.ndarray]:
         return [self.rk.phi_b.download(), self.rk.pi_b.download()]
+
+    def phi_with_ghosts(self) -> np.ndarray:
+        return self.rk.phi_b.download(with_ghosts=True)
 
 
 class C4Level:

@@ -55,11 +55,21 @@ struct BoxDesc {
 
 struct D4Params {
     BoxDesc box[SB_MAX_BOXES];
+    // RK stages (single box): TMA maps of the pointwise operands (TX x TY x 1
+    // boxes at interior coordinates), staged next to the stencil plane
+    CUtensorMap pwmap[5];
+    int pw_tma0[5][3];
+    int per[3];                // periodic extents for fused ghost stores (0 = none)
+    int pghost;                // ghost width refreshed by the fused stores
     int nbox;
     int ty, zc;
     double k1, k2, k11;
     double ca;
 };
+
+__host__ __device__ constexpr int n_pointwise(int mode) {
+    return mode == D4_RK1 ? 1 : (mode == D4_RK23 || mode == D4_RK4) ? 5 : 0;
+}
 
 // Predicated streaming stores (no branches): pair / single lanes.
 __device__ __forceinline__ void st_v2(double *p, double a, double b, int pred) {
@@ -138,10 +148,56 @@ struct Ctx {
     const double *stages;
     double *rxb;
     uint64_t *full;
-    int stage_elems, H, TY, nthr, tid, cx, ry;
+    int stage_elems, plane_elems, pw_elems, H, TY, nthr, tid, cx, ry;
     int X0, Y0, Z0, Z1, nplanes;
     long long off_xy;   // x + y*sy of the thread's first point
 };
+
+// Thread 0: arm stage s with plane j of the CTA's stream — the stencil plane
+// (with halo) and, for the RK stages once outputs start (j >= 4), the
+// pointwise operand planes of output plane Z0-4+j.
+template <int MODE, int TX>
+__device__ __forceinline__ void issue_plane(const Ctx &c, const D4Params &P, const BoxDesc &B, int j, int s) {
+    constexpr int NPW = n_pointwise(MODE);
+    double *st = const_cast<double *>(c.stages) + s * c.stage_elems;
+    const bool with_pw = NPW > 0 && j >= 4;
+    const uint32_t bytes = (uint32_t)((TX + 4) * c.H * 8 + (with_pw ? NPW * TX * c.TY * 8 : 0));
+    mbar_arrive_expect_tx(&c.full[s], bytes);
+    tma_load_3d(st, &B.tmap, B.tma0[0] + c.X0 - 2, B.tma0[1] + c.Y0 - 2, B.tma0[2] + c.Z0 - 2 + j, &c.full[s]);
+    if constexpr (NPW > 0) {
+        if (with_pw) {
+            const int zc = c.Z0 - 4 + j;
+#pragma unroll
+            for (int a = 0; a < NPW; ++a)
+                tma_load_3d(st + c.plane_elems + a * c.pw_elems, &P.pwmap[a], P.pw_tma0[a][0] + c.X0,
+                            P.pw_tma0[a][1] + c.Y0, P.pw_tma0[a][2] + zc, &c.full[s]);
+        }
+    }
+}
+
+// Store v at (x+j, y, z) and, for a periodic box, at every ghost point whose
+// periodic image it is (fused ghost refill; exact copies).
+template <int NP>
+__device__ __forceinline__ void store_periodic(double *base, long long sy, long long sz, const D4Params &P, int x,
+                                               int y, int z, const double (&v)[NP], const Lanes<NP> &L) {
+    const int g = P.pghost;
+    const int ny = P.per[1], nz = P.per[2], nx = P.per[0];
+    const int oy = y < g ? ny : (y >= ny - g ? -ny : 0);
+    const int oz = z < g ? nz : (z >= nz - g ? -nz : 0);
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+        if (!L.m[j]) continue;
+        const int xs = x + j;
+        const int ox = xs < g ? nx : (xs >= nx - g ? -nx : 0);
+        if ((ox | oy | oz) == 0) continue;
+        double *p0 = base + xs + (long long)y * sy + (long long)z * sz;
+        for (int m = 1; m < 8; ++m) {
+            const int dx = (m & 1) ? ox : 0, dy = (m & 2) ? oy : 0, dz = (m & 4) ? oz : 0;
+            if (((m & 1) && !ox) || ((m & 2) && !oy) || ((m & 4) && !oz)) continue;
+            p0[dx + (long long)dy * sy + (long long)dz * sz] = v[j];
+        }
+    }
+}
 
 template <int MODE, int TX, int NP, int R>
 __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &P, const BoxDesc &B,
@@ -153,18 +209,19 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
     const int zc = z - 2;          // plane whose z terms complete now (i >= 4)
     const long long offc = c.off_xy + (long long)zc * B.sz;
 
-    // pointwise operands of the RK stages for plane zc, issued before the wait
-    double pw[5][NP];
-    if constexpr (MODE >= D4_RK1) {
-        if (i >= 4) {
-            constexpr int np = (MODE == D4_RK1) ? 1 : 5;
-#pragma unroll
-            for (int a = 0; a < np; ++a) load<NP>(B.g[4 + a] + offc, pw[a], L);
-        }
-    }
-
     mbar_wait(&c.full[s], (i / kStages) & 1);
     const double *pl = c.stages + s * c.stage_elems;
+
+    // pointwise operands of the RK stages for plane zc (TMA-staged with the plane)
+    constexpr int NPW = n_pointwise(MODE);
+    double pw[5][NP];
+    if constexpr (NPW > 0) {
+        if (i >= 4) {
+#pragma unroll
+            for (int a = 0; a < NPW; ++a)
+                col_vals<NP>(pl + c.plane_elems + a * c.pw_elems + c.ry * TX + NP * c.cx, pw[a]);
+        }
+    }
     double xr[NP + 4], ym2[NP], ym1[NP], yp1[NP], yp2[NP];
     row_vals<NP>(pl + (c.ry + 2) * W + NP * c.cx, xr);
     col_vals<NP>(pl + (c.ry + 0) * W + NP * c.cx + 2, ym2);
@@ -213,11 +270,7 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
 
     // every thread is done with stage s (and rx of this plane is visible)
     named_bar(1, c.nthr);
-    if (c.tid == 0 && i + kStages < c.nplanes) {
-        mbar_arrive_expect_tx(&c.full[s], (uint32_t)(W * c.H * 8));
-        tma_load_3d(const_cast<double *>(pl), &B.tmap, B.tma0[0] + c.X0 - 2, B.tma0[1] + c.Y0 - 2,
-                    B.tma0[2] + c.Z0 - 2 + i + kStages, &c.full[s]);
-    }
+    if (c.tid == 0 && i + kStages < c.nplanes) issue_plane<MODE, TX>(c, P, B, i + kStages, s);
 
     if constexpr (MODE == D4_ALL10) {
         if (z >= c.Z0 && z < c.Z1) {
@@ -278,6 +331,7 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
             po[j] = add(pw[0][j], mul(cc, lap[j]));
         }
         store<NP>(B.g[0] + offc, fo, L);
+        if (P.per[0]) store_periodic<NP>(B.g[0], B.sy, B.sz, P, c.X0 + NP * c.cx, c.Y0 + c.ry, zc, fo, L);
         store<NP>(B.g[1] + offc, po, L);
         store<NP>(B.g[2] + offc, pw[0], L);
         store<NP>(B.g[3] + offc, lap, L);
@@ -304,6 +358,7 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
             }
         }
         store<NP>(B.g[0] + offc, o0, L);
+        if (P.per[0]) store_periodic<NP>(B.g[0], B.sy, B.sz, P, c.X0 + NP * c.cx, c.Y0 + c.ry, zc, o0, L);
         store<NP>(B.g[1] + offc, o1, L);
     }
     return false;
@@ -319,7 +374,9 @@ __global__ void __launch_bounds__(max_threads(MODE, NP), 1) d4_kernel(const __gr
     c.TY = P.ty;
     c.H = c.TY + 4;
     c.nthr = TPR * c.TY;
-    c.stage_elems = round_up(W * c.H, 16);
+    c.plane_elems = round_up(W * c.H, 16);
+    c.pw_elems = round_up(TX * c.TY, 16);
+    c.stage_elems = c.plane_elems + n_pointwise(MODE) * c.pw_elems;
     c.full = reinterpret_cast<uint64_t *>(smem);
     c.stages = reinterpret_cast<const double *>(smem + 128);
     c.rxb = reinterpret_cast<double *>(smem + 128) + kStages * c.stage_elems;
@@ -362,12 +419,7 @@ __global__ void __launch_bounds__(max_threads(MODE, NP), 1) d4_kernel(const __gr
         for (int s = 0; s < kStages; ++s) mbar_init(&c.full[s], 1);
         fence_mbar_init();
         tma_prefetch_desc(&B.tmap);
-        const uint32_t bytes = (uint32_t)(W * c.H * 8);
-        for (int i = 0; i < kStages && i < c.nplanes; ++i) {
-            mbar_arrive_expect_tx(&c.full[i], bytes);
-            tma_load_3d(const_cast<double *>(c.stages) + i * c.stage_elems, &B.tmap, B.tma0[0] + c.X0 - 2,
-                        B.tma0[1] + c.Y0 - 2, B.tma0[2] + c.Z0 - 2 + i, &c.full[i]);
-        }
+        for (int i = 0; i < kStages && i < c.nplanes; ++i) issue_plane<MODE, TX>(c, P, B, i, i);
     }
     __syncthreads();
 
@@ -388,7 +440,8 @@ __global__ void __launch_bounds__(max_threads(MODE, NP), 1) d4_kernel(const __gr
 
 size_t smem_bytes(int mode, int tx, int ty) {
     const int H = ty + 4;
-    size_t smem = 128 + (size_t)kStages * round_up((tx + 4) * H, 16) * 8;
+    const int stage = round_up((tx + 4) * H, 16) + n_pointwise(mode) * round_up(tx * ty, 16);
+    size_t smem = 128 + (size_t)kStages * stage * 8;
     if (mode == D4_ALL10) smem += (size_t)2 * H * tx * 8;
     return smem;
 }
@@ -483,6 +536,28 @@ int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, 
     if (nbox == 0) return SB_OK;
     if (nbox > 1 && mode != D4_LAP4) return fail(SB_USAGE, "only the Laplacian sweeps several boxes per launch");
     P.nbox = nbox;
+    const int npw = n_pointwise(mode);
+    for (int a = 0; a < npw; ++a) {
+        const sb_array &A = jobs[0].g[4 + a];
+        int rc = make_tmap(&P.pwmap[a], A, TX, TY, 1);
+        if (rc) return rc;
+        P.pw_tma0[a][0] = A.xpad;
+        P.pw_tma0[a][1] = A.ghost;
+        P.pw_tma0[a][2] = A.ghost;
+    }
+    if (npw > 0 && (p.flags & SB_LAUNCH_PERIODIC_GHOSTS)) {
+        const sb_array &O = jobs[0].g[0];
+        if (O.ghost < 1 || O.ghost > O.nx || O.ghost > O.ny || O.ghost > O.nz)
+            return fail(SB_USAGE, "periodic ghost refresh needs 1 <= ghost <= every extent of phi_out");
+        const sb_space &sp = jobs[0].space;
+        for (int d = 0; d < 3; ++d)
+            if (sp.lo[d] != 0 || sp.hi[d] != (d == 0 ? O.nx : d == 1 ? O.ny : O.nz))
+                return fail(SB_USAGE, "periodic ghost refresh needs the stage to sweep the whole interior");
+        P.per[0] = O.nx;
+        P.per[1] = O.ny;
+        P.per[2] = O.nz;
+        P.pghost = O.ghost;
+    }
     const int nb = (int)total;
     switch (mode) {
         case D4_ALL10: return launch_np<D4_ALL10>(P, TX, NP, nb, st);

@@ -196,36 +196,49 @@ class PeriodicGhosts:
 
 
 class WaveRK4:
-    """K4 + K5 — one classical RK4 step of d/dt(phi, pi) = (pi, Lap4 phi) on a
-    periodic box: four stage launches, each preceded by a periodic ghost
-    refill of the stage's phi.  State buffers are allocated once."""
+    """K5 — one classical RK4 step of d/dt(phi, pi) = (pi, Lap4 phi) on a
+    periodic box: four stage launches.  Each stage also refreshes the ghost
+    shell of the phi it produces (fused periodic refill), so after the
+    initial fill of phi0 no separate ghost kernel runs; ``fused_ghosts=False``
+    uses the stand-alone K4 refill before every stage instead.  State
+    buffers are allocated once."""
 
     site_id = "wave_rk4"
 
-    def __init__(self, n: int, ghost: int, c: WaveConstants, device=None):
+    def __init__(self, n: int, ghost: int, c: WaveConstants, device=None, fused_ghosts: bool = True):
         self.n, self.g, self.c = n, ghost, c
+        self.fused_ghosts = fused_ghosts
         mk = lambda: DeviceGrid((n, n, n), ghost, device)
         self.phi0, self.pi0 = mk(), mk()
         self.phi_a, self.pi_a, self.phi_b, self.pi_b = mk(), mk(), mk(), mk()
         self.acc_phi, self.acc_pi = mk(), mk()
-        # best of the sweep at 384^3 (profiles/r01/v2_sweep_c3.jsonl)
-        self.params = LaunchParams(128, 2, 256, 1)
+        # best of the sweep at 384^3 (profiles/r01/v3_sweep_c3_tma_pointwise_fused_ghosts.jsonl)
+        self.params = LaunchParams(64, 4, 16, 1)
+
+    def launch_space(self) -> LaunchSpace:
+        return RK4_SPACE
 
     def _consts(self) -> _lib.sb_rk4_constants:
         return _lib.sb_rk4_constants(_lib.d4_constants(self.c.lap), self.c.half_dt, self.c.dt, self.c.dt6)
 
+    def fill_ghosts(self, grid: DeviceGrid, stream=None) -> None:
+        _lib.call("sb_ghost_periodic", grid.abi(), stream_ptr(stream))
+
     def stage(self, s: int, phi_s: DeviceGrid, pi_s: DeviceGrid, phi_out: DeviceGrid, pi_out: DeviceGrid,
               params: LaunchParams, stream=None) -> None:
-        _lib.call("sb_ghost_periodic", phi_s.abi(), stream_ptr(stream))
+        if not self.fused_ghosts:
+            self.fill_ghosts(phi_s, stream)
         f = _lib.sb_rk4_fields(phi_s.abi(), pi_s.abi(), self.phi0.abi(), self.pi0.abi(), self.acc_phi.abi(),
                                self.acc_pi.abi(), phi_out.abi(), pi_out.abi())
         n = self.n
+        flags = _lib.SB_LAUNCH_PERIODIC_GHOSTS if self.fused_ghosts else 0
         _lib.call("sb_rk4_stage", s, C.byref(f), _lib.space((0, 0, 0), (n, n, n)), self._consts(),
-                  _lib.launch_of(params), stream_ptr(stream))
+                  _lib.launch_of(params, flags), stream_ptr(stream))
 
     def step(self, params: LaunchParams | None = None, stream=None) -> tuple[DeviceGrid, DeviceGrid]:
-        """One RK4 step from (phi0, pi0); returns the grids holding the new state
-        (phi0/pi0 themselves are left unchanged)."""
+        """One RK4 step from (phi0, pi0) (phi0's ghost shell must be filled;
+        see fill_ghosts); returns the grids holding the new state, whose phi
+        ghost shell is filled when fused_ghosts is on."""
         p = params or self.params
         self.stage(1, self.phi0, self.pi0, self.phi_a, self.pi_a, p, stream)
         self.stage(2, self.phi_a, self.pi_a, self.phi_b, self.pi_b, p, stream)
@@ -236,6 +249,8 @@ class WaveRK4:
     def advance(self, params: LaunchParams | None = None, stream=None) -> None:
         """Step and make the new state the start of the next step."""
         phi, pi = self.step(params, stream)
+        if not self.fused_ghosts:
+            self.fill_ghosts(phi, stream)
         self.phi0, self.phi_b = phi, self.phi0
         self.pi0, self.pi_b = pi, self.pi0
 

@@ -251,17 +251,38 @@ def test_c3_small_golden(golden):
     assert bits_equal(pi, a["c3_pi1"]), first_diff(pi, a["c3_pi1"])
 
 
-def test_c3_medium_vs_oracle():
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("params", [(64, 4, 16, 2), (128, 2, 48, 1), (32, 8, 5, 1)])
+def test_c3_medium_vs_oracle(fused, params):
+    """Interior and (fused) periodic ghost shell of phi after one RK4 step."""
     from paper_1308_1343_b200.configs import C3WaveRK4
     from paper_1308_1343_b200.tuner import LaunchParams
     n, g = 48, 2
-    p = C3WaveRK4(n=n, seed=77).setup()
-    p.run(LaunchParams(64, 4, 16))
+    p = C3WaveRK4(n=n, seed=77, fused_ghosts=fused).setup()
+    p.run(LaunchParams(*params))
     phi, pi = p.outputs()
     wphi, wpi = oracle.rk4_step(p.host_phi, p.host_pi, g, p.c)
     I = (slice(g, g + n),) * 3
     assert bits_equal(phi, wphi[I]), first_diff(phi, wphi[I])
     assert bits_equal(pi, wpi[I]), first_diff(pi, wpi[I])
+    if fused:
+        full = p.phi_with_ghosts()
+        assert bits_equal(full, wphi), first_diff(full, wphi)
+
+
+def test_c3_two_steps_advance():
+    """advance() twice equals two oracle steps (ghosts carried by the fused refill)."""
+    from paper_1308_1343_b200.configs import C3WaveRK4
+    n, g = 24, 2
+    p = C3WaveRK4(n=n, seed=5).setup()
+    p.rk.advance()
+    p.rk.advance()
+    a, b = oracle.rk4_step(p.host_phi, p.host_pi, g, p.c)
+    a, b = oracle.rk4_step(a, b, g, p.c)
+    I = (slice(g, g + n),) * 3
+    got = p.rk.phi0.download()
+    assert bits_equal(got, a[I]), first_diff(got, a[I])
+    assert bits_equal(p.rk.pi0.download(), b[I])
 
 
 def test_c3_full_size_zero_state_and_shapes_agree():
