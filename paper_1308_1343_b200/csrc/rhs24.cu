@@ -1,21 +1,27 @@
 // rhs24.cu — K6: config-5 fused many-variable right-hand side (sm_100a).
 //
 // For every interior point: 24 fields, each with its value and 9 fourth-order
-// derivatives (Dx Dy Dz Dxx Dyy Dzz Dxy Dxz Dyz — the same expression trees as
+// derivatives (Dx Dy Dz Dxx Dyy Dzz Dxy Dxz Dyz — the expression trees of
 // d4.cu), give 240 inputs v[10*var + slot]; output o is the seed-generated
 // polynomial  ((t_0 + t_1) + ...) + t_63,  t_k = (c_ok * v_p) * v_q
 // (oracle/stencils.py: rhs24).
 //
-// One CTA owns an 8x4x2 block of 64 points:
-//   phase A — TMA stages the 12x8x6 halo block of each field into a 16-slot
-//             shared-memory ring (mbarrier completion); 8 fields are reduced
-//             to their 10 slots per round (one thread per (field, point)),
-//             results into a [240][64] shared array;
-//   phase B — one thread per (point, group of 3 outputs); every lane of a
-//             warp evaluates the same term, so the (c, p, q) table is read
-//             as a uniform broadcast from __constant__ memory, and operand
-//             loads are conflict-free rows of the [240][64] array.
-// The workload is FP64-pipe / shared-memory bound, not HBM.
+// One CTA = 24 warps owns an 8 x 4 tile of (x, y) columns and streams z:
+//   * every plane of all 24 fields (tile + 2-point halo, 12 x 8) arrives by
+//     TMA (24 cp.async.bulk.tensor.3d per plane, one mbarrier) into a
+//     6-stage shared-memory ring;
+//   * phase A — warp v reduces field v, lane = column: u and the unscaled x/y
+//     first differences of the newest plane go into five-slot register rings
+//     (plane loop unrolled five ways), the x differences of the plane
+//     (with halo rows) into a 3-plane shared ring for Dxy; two planes later
+//     the ten slots of the completed plane go to a [240][32] shared array;
+//   * phase B — warp o evaluates output o for the 32 columns: every lane runs
+//     the same term, so (c, p, q) is one broadcast 16-byte shared-memory read
+//     (the table is copied to shared memory per CTA: 24 warps walking 24
+//     different 1 KB slices of __constant__ memory thrash the constant cache)
+//     and the two operand loads per term are conflict-free rows of [240][32].
+// Two CTA barriers per plane.  Bound: shared-memory bandwidth (two 8-byte
+// operand loads per term per point), then the FP64 pipe.
 #include <cstring>
 
 #include "common.cuh"
@@ -25,115 +31,186 @@ namespace sb {
 
 namespace {
 
-constexpr int PX = 8, PY = 4, PZ = 2, NPT = PX * PY * PZ;   // 64 points per CTA
-constexpr int HX = PX + 4, HY = PY + 4, HZ = PZ + 4;       // halo block 12x8x6
-constexpr int HALO = HX * HY * HZ;                          // 576 doubles
-constexpr int NSLOT = 16;                                   // staging ring
-constexpr int NTHREADS = 512;
+constexpr int TXc = 8, TYc = 4, NCOL = TXc * TYc;      // 32 columns per CTA
+constexpr int HXc = TXc + 4, HYc = TYc + 4;             // 12 x 8 halo plane
+constexpr int PLANE = HXc * HYc;                        // 96 doubles
+constexpr int NV = SB_N_VARS, NT = SB_N_TERMS;
+constexpr int NSTAGE = 5;                               // planes resident: zc .. z+2
+constexpr int NTHREADS = NV * 32;                       // 768
+
+// One polynomial term: coefficient and the byte offsets of v_p (low 16 bits)
+// and v_q (high 16 bits) in the [240][32] operand array.
+struct __align__(16) Term {
+    double c;
+    uint32_t pq;
+    uint32_t pad;
+};
+constexpr size_t SMEM_BYTES = 128 + sizeof(Term) * NV * NT +
+                              sizeof(double) * ((size_t)NSTAGE * NV * PLANE + (size_t)3 * NV * HYc * TXc +
+                                                (size_t)10 * NV * NCOL);
 
 struct PolyConst {
-    double c[SB_N_VARS][SB_N_TERMS];
-    short p[SB_N_VARS][SB_N_TERMS];
-    short q[SB_N_VARS][SB_N_TERMS];
+    Term t[NV][NT];
 };
 __constant__ PolyConst g_poly;
 
 struct Rhs24Params {
-    CUtensorMap tmap[SB_N_VARS];
-    Grid out[SB_N_VARS];
-    int tma0[SB_N_VARS][3];
+    CUtensorMap tmap[NV];
+    double *out[NV];
+    long long osy, osz;      // output strides (shared by all outputs)
+    int tma0[NV][3];
     int lo[3], hi[3];
-    int ntx, nty;
+    int ntx, nty, zc;
     double k1, k2, k11;
 };
 
-__device__ __forceinline__ void field_slots(const double *h, int px, int py, int pz, double k1, double k2,
-                                            double k11, double *vals, int var, int pt) {
-    auto H = [&](int dx, int dy, int dz) -> double {
-        return h[(pz + 2 + dz) * (HY * HX) + (py + 2 + dy) * HX + (px + 2 + dx)];
-    };
-    auto rx = [&](int dy, int dz) { return d1u(H(-2, dy, dz), H(-1, dy, dz), H(1, dy, dz), H(2, dy, dz)); };
-    auto ry = [&](int dx, int dz) { return d1u(H(dx, -2, dz), H(dx, -1, dz), H(dx, 1, dz), H(dx, 2, dz)); };
-    double *o = vals + (10 * var) * NPT + pt;
-    const double c = H(0, 0, 0);
-    o[0 * NPT] = c;
-    o[1 * NPT] = mul(rx(0, 0), k1);
-    o[2 * NPT] = mul(ry(0, 0), k1);
-    o[3 * NPT] = mul(d1u(H(0, 0, -2), H(0, 0, -1), H(0, 0, 1), H(0, 0, 2)), k1);
-    o[4 * NPT] = d2(H(-2, 0, 0), H(-1, 0, 0), c, H(1, 0, 0), H(2, 0, 0), k2);
-    o[5 * NPT] = d2(H(0, -2, 0), H(0, -1, 0), c, H(0, 1, 0), H(0, 2, 0), k2);
-    o[6 * NPT] = d2(H(0, 0, -2), H(0, 0, -1), c, H(0, 0, 1), H(0, 0, 2), k2);
-    o[7 * NPT] = mul(d1u(rx(-2, 0), rx(-1, 0), rx(1, 0), rx(2, 0)), k11);
-    o[8 * NPT] = mul(d1u(rx(0, -2), rx(0, -1), rx(0, 1), rx(0, 2)), k11);
-    o[9 * NPT] = mul(d1u(ry(0, -2), ry(0, -1), ry(0, 1), ry(0, 2)), k11);
+struct Ctx {
+    uint64_t *full;          // NSTAGE mbarriers
+    const Term *terms;       // [NV][NT] copy of the table in shared memory (broadcast reads)
+    double *ring;            // [NSTAGE][NV][PLANE]
+    double *rxb;             // [3][NV][HYc][TXc]
+    double *vals;            // [240][NCOL]
+    int tid, warp, lane, cx, cy;
+    int X0, Y0, Z0, Z1, nplanes;
+    bool active;
+};
+
+struct Rings {
+    double u[5], rx[5], ry[5];
+};
+
+// thread 0: all 24 field planes of stream plane j into stage j % NSTAGE
+__device__ __forceinline__ void issue(const Rhs24Params &P, const Ctx &c, int j) {
+    const int s = j % NSTAGE;
+    mbar_arrive_expect_tx(&c.full[s], NV * PLANE * 8);
+    double *dst = c.ring + s * NV * PLANE;
+#pragma unroll 4
+    for (int v = 0; v < NV; ++v)
+        tma_load_3d(dst + v * PLANE, &P.tmap[v], P.tma0[v][0] + c.X0 - 2, P.tma0[v][1] + c.Y0 - 2,
+                    P.tma0[v][2] + c.Z0 - 2 + j, &c.full[s]);
+}
+
+template <int R>
+__device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c, Rings &rg) {
+    if (i >= c.nplanes) return true;
+    const int s = i % NSTAGE;
+    const int v = c.warp;   // phase A: this warp's field
+    mbar_wait(&c.full[s], (i / NSTAGE) & 1);
+
+    // ---- phase A, newest plane z = Z0-2+i: u, rx, ry into the rings; rx plane (+ halo rows) ----
+    {
+        const double *pl = c.ring + (s * NV + v) * PLANE;
+        const double *row = pl + (c.cy + 2) * HXc + c.cx;
+        const double *col = pl + c.cy * HXc + c.cx + 2;
+        rg.u[R] = row[2];
+        rg.rx[R] = d1u(row[0], row[1], row[3], row[4]);
+        rg.ry[R] = d1u(col[0], col[HXc], col[3 * HXc], col[4 * HXc]);
+        double *rxs = c.rxb + ((i % 3) * NV + v) * (HYc * TXc);
+        rxs[(c.cy + 2) * TXc + c.cx] = rg.rx[R];
+        const int h = c.lane >> 3, hc = c.lane & 7;      // lanes double as 4 halo rows x 8 columns
+        const int hr = h < 2 ? h : TYc + h;
+        const double *hrow = pl + hr * HXc + hc;
+        rxs[hr * TXc + hc] = d1u(hrow[0], hrow[1], hrow[3], hrow[4]);
+    }
+
+    // ---- phase A, completed plane zc = z-2: the ten slots ----
+    const bool out_plane = i >= 4;
+    if (out_plane) {
+        __syncwarp();    // rx plane of zc was written by this warp two planes ago; keep lanes in step
+        constexpr int K0 = (R + 1) % 5, K1 = (R + 2) % 5, K2 = (R + 3) % 5, K3 = (R + 4) % 5, K4 = R;
+        const int sc = (i - 2) % NSTAGE;
+        const double *pl = c.ring + (sc * NV + v) * PLANE;
+        const double *row = pl + (c.cy + 2) * HXc + c.cx;
+        const double *col = pl + c.cy * HXc + c.cx + 2;
+        const double uc = rg.u[K2];
+        const double *rxs = c.rxb + (((i - 2) % 3) * NV + v) * (HYc * TXc) + c.cx;
+        double *o = c.vals + (10 * v) * NCOL + c.lane;
+        o[0 * NCOL] = uc;
+        o[1 * NCOL] = mul(rg.rx[K2], P.k1);
+        o[2 * NCOL] = mul(rg.ry[K2], P.k1);
+        o[3 * NCOL] = mul(d1u(rg.u[K0], rg.u[K1], rg.u[K3], rg.u[K4]), P.k1);
+        o[4 * NCOL] = d2(row[0], row[1], uc, row[3], row[4], P.k2);
+        o[5 * NCOL] = d2(col[0], col[HXc], uc, col[3 * HXc], col[4 * HXc], P.k2);
+        o[6 * NCOL] = d2(rg.u[K0], rg.u[K1], uc, rg.u[K3], rg.u[K4], P.k2);
+        o[7 * NCOL] = mul(d1u(rxs[(c.cy + 0) * TXc], rxs[(c.cy + 1) * TXc], rxs[(c.cy + 3) * TXc],
+                              rxs[(c.cy + 4) * TXc]),
+                          P.k11);
+        o[8 * NCOL] = mul(d1u(rg.rx[K0], rg.rx[K1], rg.rx[K3], rg.rx[K4]), P.k11);
+        o[9 * NCOL] = mul(d1u(rg.ry[K0], rg.ry[K1], rg.ry[K3], rg.ry[K4]), P.k11);
+    }
+
+    // every slot of plane zc is written; the stage of the oldest plane still
+    // held is no longer read: planes 0 and 1 (halo planes, phase A1 only) after
+    // their own iteration, plane i-2 after its slots at iteration i >= 4
+    __syncthreads();
+    const int freed = i < 2 ? i : (i >= 4 ? i - 2 : -1);
+    if (c.tid == 0 && freed >= 0 && freed + NSTAGE < c.nplanes) issue(P, c, freed + NSTAGE);
+    if (!out_plane) return false;
+
+    // ---- phase B: output o = warp for the 32 columns of plane zc ----
+    {
+        const Term *tt = c.terms + c.warp * NT;
+        const char *vb = reinterpret_cast<const char *>(c.vals + c.lane);
+        auto V = [vb](uint32_t off) { return *reinterpret_cast<const double *>(vb + off); };
+        Term t0 = tt[0];
+        double acc = mul(mul(t0.c, V(t0.pq & 0xffffu)), V(t0.pq >> 16));
+#pragma unroll 16
+        for (int k = 1; k < NT; ++k) {
+            const Term tk = tt[k];
+            acc = add(acc, mul(mul(tk.c, V(tk.pq & 0xffffu)), V(tk.pq >> 16)));
+        }
+        if (c.active) {
+            const int zc = c.Z0 - 4 + i;
+            P.out[c.warp][(c.X0 + c.cx) + (long long)(c.Y0 + c.cy) * P.osy + (long long)zc * P.osz] = acc;
+        }
+    }
+    __syncthreads();   // the [240][32] array is rewritten by the next plane
+    return false;
 }
 
 __global__ void __launch_bounds__(NTHREADS, 1) rhs24_kernel(const __grid_constant__ Rhs24Params P) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
-    double *ring = reinterpret_cast<double *>(smem + 256);        // NSLOT x HALO
-    double *vals = ring + NSLOT * HALO;                            // [240][64]
-
+    Ctx c;
+    c.full = reinterpret_cast<uint64_t *>(smem);
+    Term *terms = reinterpret_cast<Term *>(smem + 128);
+    c.terms = terms;
+    c.ring = reinterpret_cast<double *>(terms + NV * NT);
+    c.rxb = c.ring + NSTAGE * NV * PLANE;
+    c.vals = c.rxb + 3 * NV * HYc * TXc;
+    c.tid = threadIdx.x;
+    c.warp = c.tid >> 5;
+    c.lane = c.tid & 31;
+    c.cx = c.lane & 7;
+    c.cy = c.lane >> 3;
     int t = blockIdx.x;
     const int bx = t % P.ntx;
     t /= P.ntx;
     const int by = t % P.nty;
     const int bz = t / P.nty;
-    const int X0 = P.lo[0] + bx * PX, Y0 = P.lo[1] + by * PY, Z0 = P.lo[2] + bz * PZ;
-    const int tid = threadIdx.x;
-    const uint32_t bytes = HALO * 8;
+    c.X0 = P.lo[0] + bx * TXc;
+    c.Y0 = P.lo[1] + by * TYc;
+    c.Z0 = P.lo[2] + bz * P.zc;
+    c.Z1 = min(c.Z0 + P.zc, P.hi[2]);
+    c.nplanes = c.Z1 - c.Z0 + 4;
+    c.active = (c.X0 + c.cx < P.hi[0]) && (c.Y0 + c.cy < P.hi[1]);
 
-    if (tid == 0) {
-        for (int s = 0; s < NSLOT; ++s) mbar_init(&bar[s], 1);
+    if (c.tid == 0) {
+        for (int s = 0; s < NSTAGE; ++s) mbar_init(&c.full[s], 1);
         fence_mbar_init();
+        for (int j = 0; j < NSTAGE && j < c.nplanes; ++j) issue(P, c, j);
     }
-    __syncthreads();
-    if (tid == 0) {
-        for (int v = 0; v < NSLOT; ++v) {
-            mbar_arrive_expect_tx(&bar[v], bytes);
-            tma_load_3d(ring + v * HALO, &P.tmap[v], P.tma0[v][0] + X0 - 2, P.tma0[v][1] + Y0 - 2,
-                        P.tma0[v][2] + Z0 - 2, &bar[v]);
-        }
-    }
-
-    // ---- phase A: 10 slots of every field ----
-    const int vo = tid / NPT;     // 0..7
-    const int pt = tid % NPT;
-    const int px = pt % PX, py = (pt / PX) % PY, pz = pt / (PX * PY);
-    for (int r = 0; r < 3; ++r) {
-        const int v = r * 8 + vo;
-        const int s = v % NSLOT;
-        mbar_wait(&bar[s], r == 2 ? 1u : 0u);
-        field_slots(ring + s * HALO, px, py, pz, P.k1, P.k2, P.k11, vals, v, pt);
-        if (r == 0) {
-            __syncthreads();   // slots 0..7 consumed: refill with fields 16..23
-            if (tid == 0) {
-                for (int v2 = 16; v2 < SB_N_VARS; ++v2) {
-                    const int s2 = v2 % NSLOT;
-                    mbar_arrive_expect_tx(&bar[s2], bytes);
-                    tma_load_3d(ring + s2 * HALO, &P.tmap[v2], P.tma0[v2][0] + X0 - 2, P.tma0[v2][1] + Y0 - 2,
-                                P.tma0[v2][2] + Z0 - 2, &bar[s2]);
-                }
-            }
-        }
-    }
+    for (int e = c.tid; e < NV * NT; e += NTHREADS) terms[e] = (&g_poly.t[0][0])[e];
     __syncthreads();
 
-    // ---- phase B: the 24 polynomials ----
-    const int og = tid / NPT;     // outputs 3*og .. 3*og+2
-    const int x = X0 + px, y = Y0 + py, z = Z0 + pz;
-    const bool active = x < P.hi[0] && y < P.hi[1] && z < P.hi[2];
-    const double *vp = vals + pt;
-#pragma unroll 1
-    for (int oo = 0; oo < 3; ++oo) {
-        const int o = 3 * og + oo;
-        double acc = mul(mul(g_poly.c[o][0], vp[g_poly.p[o][0] * NPT]), vp[g_poly.q[o][0] * NPT]);
-#pragma unroll 8
-        for (int k = 1; k < SB_N_TERMS; ++k) {
-            const double tk = mul(mul(g_poly.c[o][k], vp[g_poly.p[o][k] * NPT]), vp[g_poly.q[o][k] * NPT]);
-            acc = add(acc, tk);
-        }
-        if (active) *P.out[o].at(x, y, z) = acc;
+    Rings rg;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) rg.u[k] = rg.rx[k] = rg.ry[k] = 0.0;
+    for (int i = 0;; i += 5) {
+        if (plane<0>(i + 0, P, c, rg)) break;
+        if (plane<1>(i + 1, P, c, rg)) break;
+        if (plane<2>(i + 2, P, c, rg)) break;
+        if (plane<3>(i + 3, P, c, rg)) break;
+        if (plane<4>(i + 4, P, c, rg)) break;
     }
 }
 
@@ -154,20 +231,22 @@ uint64_t fnv1a(const void *data, size_t n, uint64_t h) {
 
 int launch_rhs24(const sb_array *in, const sb_array *out, const sb_space &sp, const sb_d4_constants &k,
                  const sb_poly &poly, const sb_launch &p, cudaStream_t st) {
-    (void)p;
     for (int d = 0; d < 3; ++d)
         if (sp.hi[d] <= sp.lo[d]) return SB_OK;
     if (!poly.coef || !poly.p || !poly.q) return fail(SB_USAGE, "rhs24: null polynomial table");
+    for (int v = 1; v < NV; ++v)
+        if (out[v].sy != out[0].sy || out[v].sz != out[0].sz)
+            return fail(SB_USAGE, "rhs24: all outputs must share row and plane strides");
 
     static PolyConst host;
-    for (int o = 0; o < SB_N_VARS; ++o)
-        for (int t = 0; t < SB_N_TERMS; ++t) {
-            const int pi = poly.p[o * SB_N_TERMS + t], qi = poly.q[o * SB_N_TERMS + t];
-            if (pi < 0 || pi >= 10 * SB_N_VARS || qi < 0 || qi >= 10 * SB_N_VARS)
+    for (int o = 0; o < NV; ++o)
+        for (int t = 0; t < NT; ++t) {
+            const int pi = poly.p[o * NT + t], qi = poly.q[o * NT + t];
+            if (pi < 0 || pi >= 10 * NV || qi < 0 || qi >= 10 * NV)
                 return fail(SB_USAGE, "rhs24: polynomial input index outside 0..239");
-            host.c[o][t] = poly.coef[o * SB_N_TERMS + t];
-            host.p[o][t] = (short)pi;
-            host.q[o][t] = (short)qi;
+            host.t[o][t].c = poly.coef[o * NT + t];
+            host.t[o][t].pq = (uint32_t)(pi * NCOL * 8) | ((uint32_t)(qi * NCOL * 8) << 16);
+            host.t[o][t].pad = 0;
         }
     const uint64_t fp = fnv1a(&host, sizeof(host), 1469598103934665603ULL);
     if (!g_poly_valid || fp != g_poly_fp) {
@@ -183,30 +262,33 @@ int launch_rhs24(const sb_array *in, const sb_array *out, const sb_space &sp, co
 
     Rhs24Params P;
     memset(&P, 0, sizeof(P));
-    for (int v = 0; v < SB_N_VARS; ++v) {
-        int rc = make_tmap(&P.tmap[v], in[v], HX, HY, HZ);
+    for (int v = 0; v < NV; ++v) {
+        int rc = make_tmap(&P.tmap[v], in[v], HXc, HYc, 1);
         if (rc) return rc;
         P.tma0[v][0] = in[v].xpad;
         P.tma0[v][1] = in[v].ghost;
         P.tma0[v][2] = in[v].ghost;
-        P.out[v] = grid_of(out[v]);
+        P.out[v] = out[v].origin;
     }
+    P.osy = out[0].sy;
+    P.osz = out[0].sz;
     for (int d = 0; d < 3; ++d) {
         P.lo[d] = sp.lo[d];
         P.hi[d] = sp.hi[d];
     }
-    P.ntx = (sp.hi[0] - sp.lo[0] + PX - 1) / PX;
-    P.nty = (sp.hi[1] - sp.lo[1] + PY - 1) / PY;
-    const int ntz = (sp.hi[2] - sp.lo[2] + PZ - 1) / PZ;
+    P.zc = p.z_chunk > 0 ? p.z_chunk : 32;
+    P.ntx = (sp.hi[0] - sp.lo[0] + TXc - 1) / TXc;
+    P.nty = (sp.hi[1] - sp.lo[1] + TYc - 1) / TYc;
+    const int ntz = (sp.hi[2] - sp.lo[2] + P.zc - 1) / P.zc;
     P.k1 = k.k1;
     P.k2 = k.k2;
     P.k11 = k.k11;
     const long long nblocks = (long long)P.ntx * P.nty * ntz;
     if (nblocks > 0x7fffffffLL) return fail(SB_RESOURCE, "rhs24: too many tiles");
-    const size_t smem = 256 + (size_t)NSLOT * HALO * 8 + (size_t)10 * SB_N_VARS * NPT * 8;
-    cudaError_t e = cudaFuncSetAttribute(rhs24_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(rhs24_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(rhs24)");
-    rhs24_kernel<<<(unsigned)nblocks, NTHREADS, smem, st>>>(P);
+    rhs24_kernel<<<(unsigned)nblocks, NTHREADS, SMEM_BYTES, st>>>(P);
     return check_cuda(cudaGetLastError(), "rhs24_kernel launch");
 }
 

@@ -259,8 +259,10 @@ class Rhs24(DeviceKernel):
     """K6 — config-5 fused 24-variable right-hand side."""
 
     site_id = "rhs24"
-    space_kind = LaunchSpace(kind="rhs24", max_threads_pair=512, points=(2,))
-    default_params = LaunchParams(64, 8, 32)   # fixed 8x4x2 point blocks; params unused
+    # the CTA shape is fixed (8 x 4 columns, one warp per field / output =
+    # 768 threads, written here as a 32 x 24 scalar tile); only z_chunk is tuned
+    space_kind = LaunchSpace(kind="rhs24", tile_xs=(32,), tile_ys=(24,), points=(1,), max_threads_scalar=768)
+    default_params = LaunchParams(32, 24, 192, 1)   # profiles/r01/v2_sweep_c5.jsonl
 
     def __init__(self, ins: list[DeviceGrid], outs: list[DeviceGrid], k: D4Constants, poly: PolyTable):
         if len(ins) != N_VARS or len(outs) != N_VARS:
