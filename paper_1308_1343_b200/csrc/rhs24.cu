@@ -285,9 +285,13 @@ int launch_rhs24(const sb_array *in, const sb_array *out, const sb_space &sp, co
     P.k11 = k.k11;
     const long long nblocks = (long long)P.ntx * P.nty * ntz;
     if (nblocks > 0x7fffffffLL) return fail(SB_RESOURCE, "rhs24: too many tiles");
-    cudaError_t e =
-        cudaFuncSetAttribute(rhs24_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-    if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(rhs24)");
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e =
+            cudaFuncSetAttribute(rhs24_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+        if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(rhs24)");
+        configured = true;
+    }
     rhs24_kernel<<<(unsigned)nblocks, NTHREADS, SMEM_BYTES, st>>>(P);
     return check_cuda(cudaGetLastError(), "rhs24_kernel launch");
 }

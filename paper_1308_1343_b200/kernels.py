@@ -72,7 +72,8 @@ class Laplacian7(DeviceKernel):
 
     site_id = "laplacian3d"
     space_kind = LAP7_SPACE
-    default_params = LaunchParams(64, 8, 16)
+    # best of the CUDA-graph sweep at 64^3 (profiles/r01/v2_sweep_c1_graph.jsonl)
+    default_params = LaunchParams(64, 8, 4)
 
     def __init__(self, dst: DeviceGrid, src: DeviceGrid, c0: float, c1: float):
         if src.ghost < 1:

@@ -88,6 +88,44 @@ def run_tuned(n: int, iters: int, seed: int, topo: TopologyConfig, c0: float = C
     return out, tuner
 
 
+def run_graphed(n: int, iters: int, seed: int, c0: float = C0, c1: float = C1, batch: int = 50) -> StencilRun:
+    """``run_serial`` with the sweep loop captured in a CUDA graph: one graph
+    holds ``batch`` ping-pong pairs (2*batch sweeps); iter_seconds are the
+    per-sweep averages of each replay (CUDA events)."""
+    from .graphs import SweepGraph
+    if iters % 2:
+        raise ValueError("run_graphed needs an even iteration count (ping-pong pairs)")
+    a, b = _buffers(n, seed)
+    space = _space(n)
+    ka, kb = Laplacian7(b, a, c0, c1), Laplacian7(a, b, c0, c1)
+
+    def pair():
+        ka.launch(space, ka.default_params)
+        kb.launch(space, kb.default_params)
+
+    out = StencilRun(np.empty(0))
+    pairs = iters // 2
+    # the warm-up pair inside SweepGraph advances the state; start from the field again
+    g = SweepGraph(pair, repeat=min(batch, max(1, pairs)), warmup=1)
+    host = make_field(n, seed)
+    a.upload(host, with_ghosts=True)
+    b.upload(host, with_ghosts=True)
+    done = 0
+    while done < pairs:
+        if pairs - done >= g.repeat:
+            with _Timer(True) as tm:
+                g.replay()
+            out.iter_seconds += [tm.elapsed() / (2 * g.repeat)] * (2 * g.repeat)
+            done += g.repeat
+        else:
+            with _Timer(True) as tm:
+                pair()
+            out.iter_seconds += [tm.elapsed() / 2] * 2
+            done += 1
+    out.final = a.download(with_ghosts=True)
+    return out
+
+
 def bit_identical(a: np.ndarray, b: np.ndarray) -> bool:
     """stencil.py:97-98."""
     return a.shape == b.shape and a.tobytes() == b.tobytes()

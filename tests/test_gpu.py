@@ -79,6 +79,18 @@ def test_reference_demo_drivers_bit_identical(golden):
     assert len(tuner.log) == d["n64_iters"]
 
 
+def test_graphed_demo_matches_reference(golden):
+    """The CUDA-graph-captured sweep loop gives the reference's bits."""
+    from paper_1308_1343_b200 import stencil
+    meta, a = golden
+    d = meta["demo"]
+    g = stencil.run_graphed(64, d["n64_iters"], d["seed"], batch=16)
+    assert inputs.sha256(g.final) == d["n64_final_sha256"]
+    assert len(g.iter_seconds) == d["n64_iters"]
+    g16 = stencil.run_graphed(16, d["n16_iters"], d["seed"], batch=3)
+    assert bits_equal(g16.final, a["demo16_final"])
+
+
 def test_lap7_masked_subspace_writes_only_inside():
     """Odd x origin, ragged extents: only points of the space change (the
     iterate_masked frame rule)."""

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--shapes", default="all")
     ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--graph", action="store_true", help="time reps launches captured in one CUDA graph")
     args = ap.parse_args()
 
     import torch
@@ -60,14 +61,27 @@ def main():
         same = all(torch.equal(a, b) for a, b in zip(ref, got))
         for _ in range(3):
             prob.run(p)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.reps + 1)]
-        ev[0].record()
-        for i in range(args.reps):
-            prob.run(p)
-            ev[i + 1].record()
-        torch.cuda.synchronize()
-        ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.reps)]
-        med = statistics.median(ms)
+        if args.graph:
+            from paper_1308_1343_b200.graphs import SweepGraph
+            g = SweepGraph(lambda: prob.run(p), repeat=args.reps)
+            ms = []
+            for _ in range(5):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                g.replay()
+                b.record()
+                torch.cuda.synchronize()
+                ms.append(a.elapsed_time(b) / args.reps)
+            med = statistics.median(ms)
+        else:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.reps + 1)]
+            ev[0].record()
+            for i in range(args.reps):
+                prob.run(p)
+                ev[i + 1].record()
+            torch.cuda.synchronize()
+            ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.reps)]
+            med = statistics.median(ms)
         r = {"shape": p.flat(), "ms": med, "gpts": prob.updates / med / 1e6,
              "gbs": prob.canonical_bytes / med / 1e6, "bits_equal": same}
         results.append(r)
