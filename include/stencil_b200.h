@@ -130,6 +130,19 @@ typedef struct sb_poly {
     const int32_t *q;
 } sb_poly;
 
+/* One region copy between two grids of a level (inter-box ghost fill):
+ * dst[dst_lo + i] = src[src_lo + i] for 0 <= i < ext, coordinates relative to
+ * each grid's interior origin (dst_lo may lie in the ghost zone). */
+typedef struct sb_copy_job {
+    sb_array dst;
+    sb_array src;
+    int32_t dst_lo[3];
+    int32_t src_lo[3];
+    int32_t ext[3];
+} sb_copy_job;
+
+#define SB_MAX_COPY_JOBS 64   /* region copies per launch (sb_copy_regions) */
+
 typedef struct sb_device_info {
     int32_t device, sm_count, cc_major, cc_minor;
     int64_t l2_bytes, smem_optin_bytes, global_mem_bytes;
@@ -174,6 +187,11 @@ SB_API int sb_rk4_stage(int32_t stage, const sb_rk4_fields *f, sb_space space,
 /* K6 — config-5 fused right-hand side: 24 inputs (ghost >= 2) -> 24 outputs. */
 SB_API int sb_rhs24(const sb_array *in, const sb_array *out, sb_space space,
              sb_d4_constants k, sb_poly poly, sb_launch p, void *stream);
+
+/* F1 — inter-box ghost fill of a refinement level: every region copy of the
+ * schedule (built on the host from the level's boxes, level.ghost_schedule)
+ * in one launch; pure copies, bit-exact. */
+SB_API int sb_copy_regions(const sb_copy_job *jobs, int32_t njobs, void *stream);
 
 /* Host <-> device transfer of a whole ghosted grid (with_ghosts = 1) or of
  * its interior (0).  `host` is dense (z,y,x), x contiguous. */

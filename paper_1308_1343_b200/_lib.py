@@ -27,8 +27,9 @@ SB_N_TERMS = 64
 EXPORTS = (
     "sb_abi_version", "sb_last_error", "sb_init", "sb_get_device_info", "sb_diff1d",
     "sb_lap7", "sb_d4_all", "sb_lap4_boxes", "sb_ghost_periodic", "sb_rk4_stage",
-    "sb_rhs24", "sb_copy_h2d", "sb_copy_d2h",
+    "sb_rhs24", "sb_copy_regions", "sb_copy_h2d", "sb_copy_d2h",
 )
+SB_MAX_COPY_JOBS = 64
 
 
 class sb_array(C.Structure):
@@ -65,6 +66,11 @@ class sb_poly(C.Structure):
     _fields_ = [("coef", C.c_void_p), ("p", C.c_void_p), ("q", C.c_void_p)]
 
 
+class sb_copy_job(C.Structure):
+    _fields_ = [("dst", sb_array), ("src", sb_array), ("dst_lo", C.c_int32 * 3), ("src_lo", C.c_int32 * 3),
+                ("ext", C.c_int32 * 3)]
+
+
 class sb_device_info(C.Structure):
     _fields_ = [("device", C.c_int32), ("sm_count", C.c_int32), ("cc_major", C.c_int32), ("cc_minor", C.c_int32),
                 ("l2_bytes", C.c_int64), ("smem_optin_bytes", C.c_int64), ("global_mem_bytes", C.c_int64)]
@@ -89,6 +95,7 @@ def _declare(lib) -> None:
         "sb_rk4_stage": ([i32, C.POINTER(sb_rk4_fields), sb_space, sb_rk4_constants, sb_launch, vp], C.c_int),
         "sb_rhs24": ([C.POINTER(sb_array), C.POINTER(sb_array), sb_space, sb_d4_constants, sb_poly, sb_launch, vp],
                      C.c_int),
+        "sb_copy_regions": ([C.POINTER(sb_copy_job), i32, vp], C.c_int),
         "sb_copy_h2d": ([sb_array, vp, i32, vp], C.c_int),
         "sb_copy_d2h": ([vp, sb_array, i32, vp], C.c_int),
     }

@@ -14,7 +14,7 @@ import numpy as np
 
 from . import inputs
 from .grid import DeviceGrid
-from .kernels import FourthOrderAll, Laplacian7, LevelLaplacian4, Rhs24, WaveRK4
+from .kernels import FourthOrderAll, Laplacian7, LevelGhostSync, LevelLaplacian4, Rhs24, WaveRK4
 from .level import Box, box_difference
 from .traverse import IndexSpace
 from .tuner import LaunchParams
@@ -158,6 +158,7 @@ class C4Level:
             self.srcs.append(s)
             self.dsts.append(DeviceGrid(b.extents, 0, device, lower=b.lo))
         self.kernel = LevelLaplacian4(self.dsts, self.srcs, self.k)
+        self.ghost_sync = LevelGhostSync(self.srcs, self.boxes)
         return self
 
     def run(self, params: LaunchParams | None = None, stream=None) -> None:

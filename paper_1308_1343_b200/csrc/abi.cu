@@ -249,6 +249,15 @@ int sb_rhs24(const sb_array *in, const sb_array *out, sb_space space, sb_d4_cons
     return launch_rhs24(in, out, space, k, poly, p, as_stream(stream));
 }
 
+int sb_copy_regions(const sb_copy_job *jobs, int32_t njobs, void *stream) {
+    if (njobs > 0 && !jobs) return fail(SB_USAGE, "copy_regions: null job table");
+    int rc;
+    for (int j = 0; j < njobs; ++j)
+        if ((rc = check_array(jobs[j].dst, 0, "copy_regions dst")) || (rc = check_array(jobs[j].src, 0, "copy_regions src")))
+            return rc;
+    return launch_copy_regions(jobs, njobs, as_stream(stream));
+}
+
 int sb_copy_h2d(sb_array dst, const double *host, int32_t with_ghosts, void *stream) {
     int rc = check_array(dst, 0, "copy_h2d");
     if (rc) return rc;

@@ -186,6 +186,42 @@ class LevelLaplacian4(DeviceKernel):
         self._run(self._jobs(piece), self.default_params, None)
 
 
+class LevelGhostSync:
+    """F1 — fill every box's ghost zone from the interiors of the other boxes
+    of its level (schedule: level.ghost_schedule), all copies of a chunk of
+    up to SB_MAX_COPY_JOBS regions in one launch."""
+
+    def __init__(self, grids: list[DeviceGrid], boxes=None):
+        from .level import Box, ghost_schedule
+        if not grids:
+            raise UsageError("need at least one grid")
+        g = min(d.ghost for d in grids)
+        if boxes is None:
+            boxes = [Box(d.lower, tuple(l + e - 1 for l, e in zip(d.lower, d.extents))) for d in grids]
+        self.grids = list(grids)
+        self.schedule = ghost_schedule(list(boxes), g)
+        jobs = []
+        for c in self.schedule:
+            dst, src = self.grids[c.dst], self.grids[c.src]
+            j = _lib.sb_copy_job()
+            j.dst, j.src = dst.abi(), src.abi()
+            for d in range(3):
+                j.dst_lo[d] = c.region.lo[d] - dst.lower[d]
+                j.src_lo[d] = c.region.lo[d] - src.lower[d]
+                j.ext[d] = c.region.hi[d] - c.region.lo[d] + 1
+            jobs.append(j)
+        self._jobs = jobs
+
+    def points(self) -> int:
+        return sum(c.region.volume() for c in self.schedule)
+
+    def __call__(self, stream=None) -> None:
+        for i in range(0, len(self._jobs), _lib.SB_MAX_COPY_JOBS):
+            chunk = self._jobs[i:i + _lib.SB_MAX_COPY_JOBS]
+            arr = (_lib.sb_copy_job * len(chunk))(*chunk)
+            _lib.call("sb_copy_regions", arr, len(chunk), stream_ptr(stream))
+
+
 class PeriodicGhosts:
     """K4 — periodic refill of a grid's ghost shell."""
 

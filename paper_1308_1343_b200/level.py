@@ -111,3 +111,42 @@ def box_difference(a: Box, b: Box) -> list[Box]:
         cur_lo[d], cur_hi[d] = lo[d], hi[d]
     key = lambda bx: (tuple(reversed(bx.lo)), tuple(reversed(bx.hi)))
     return sorted(pieces, key=key)
+
+
+def intersect(a: Box, b: Box) -> Box:
+    lo = tuple(max(x, y) for x, y in zip(a.lo, b.lo))
+    hi = tuple(min(x, y) for x, y in zip(a.hi, b.hi))
+    return Box(lo, hi) if all(l <= h for l, h in zip(lo, hi)) else Box.empty(a.dim)
+
+
+def expand(b: Box, g: int) -> Box:
+    """Grow a box by g points on every face (the reference's BBox expand,
+    lattice.py:156-191, at unit stride)."""
+    return Box(tuple(v - g for v in b.lo), tuple(v + g for v in b.hi))
+
+
+@dataclass(frozen=True)
+class GhostCopy:
+    """Ghost points of box `dst` that lie in the interior of box `src`."""
+
+    dst: int
+    src: int
+    region: Box
+
+
+def ghost_schedule(boxes: list[Box], g: int) -> list[GhostCopy]:
+    """The inter-box ghost-fill schedule of a level:
+    for every ordered pair of distinct boxes, expand(dst, g) ∩ src.  Boxes of
+    a level are disjoint, so each such region lies in dst's ghost zone and in
+    src's interior; ghost points outside every box (the level boundary) are
+    not touched."""
+    out = []
+    for i, a in enumerate(boxes):
+        grown = expand(a, g)
+        for j, b in enumerate(boxes):
+            if i == j:
+                continue
+            r = intersect(grown, b)
+            if not r.is_empty:
+                out.append(GhostCopy(i, j, r))
+    return out

@@ -196,6 +196,20 @@ def level_boxes(n):
     return [[list(b.lower.coords), list(b.upper.coords)] for b in boxes]
 
 
+def ghost_regions(n, g):
+    """Per box of the level, the reference bboxset algebra's ghost-sync
+    region: (expand(box, g) ∩ level) \\ box, as its canonical box list."""
+    outer = BBox(Point((0, 0, 0)), Point((n - 1,) * 3), Stride.ones(3))
+    hole = BBox(Point((n // 2,) * 3), Point((n - 1,) * 3), Stride.ones(3))
+    lvl = BBoxSet.from_bboxes([outer]).difference(BBoxSet.from_bboxes([hole]))
+    out = []
+    for b in lvl.to_bboxes():
+        grown = BBoxSet.from_bboxes([b.expand(Point((g,) * 3), Point((g,) * 3))])
+        ghost = grown.intersection(lvl).difference(BBoxSet.from_bboxes([b]))
+        out.append([[list(r.lower.coords), list(r.upper.coords)] for r in ghost.to_bboxes()])
+    return out
+
+
 def golden_c4(n=16, g=2):
     from paper_1308_1343_b200.level import Box
     boxes = [Box(tuple(lo), tuple(hi)) for lo, hi in level_boxes(n)]
@@ -356,6 +370,7 @@ def main():
     meta["c4"] = {"n": 16, "g": 2, "seed": inputs.seed_for(4) + 1000,
                   "boxes": [[list(b.lo), list(b.hi)] for b in boxes]}
     meta["c4_level512_boxes"] = level_boxes(512)
+    meta["c4_ghost_regions_n12_g2"] = ghost_regions(12, 2)
 
     f5, poly5, o5 = golden_c5()
     arrays["c5_in"] = np.stack(f5)

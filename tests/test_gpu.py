@@ -362,3 +362,32 @@ def test_bad_launch_params_raise_usage_error():
         p.run(LaunchParams(48, 4, 4))
     with pytest.raises(UsageError):
         p.run(LaunchParams(64, 16, 4))   # 512 consumer threads > d4_all limit
+
+
+def test_level_ghost_sync_matches_global_field():
+    """F1: after the inter-box ghost fill every ghost point that lies inside
+    the level equals the neighbouring box's interior value; others untouched."""
+    from paper_1308_1343_b200.configs import C4Level
+    n, g = 40, 2
+    p = C4Level(n=n, seed=3).setup()
+    glob = np.full((n, n, n), np.nan)
+    for b, u in zip(p.boxes, p.host_u):
+        nx, ny, nz = b.extents
+        glob[b.lo[2]:b.hi[2] + 1, b.lo[1]:b.hi[1] + 1, b.lo[0]:b.hi[0] + 1] = u[g:g + nz, g:g + ny, g:g + nx]
+    p.ghost_sync()
+    assert p.ghost_sync.points() > 0
+    for b, u, s in zip(p.boxes, p.host_u, p.srcs):
+        got = s.download(with_ghosts=True)
+        want = u.copy()
+        nx, ny, nz = b.extents
+        for kz in range(nz + 2 * g):
+            for ky in range(ny + 2 * g):
+                z, y = b.lo[2] - g + kz, b.lo[1] - g + ky
+                if not (0 <= z < n and 0 <= y < n):
+                    continue
+                xs = np.arange(b.lo[0] - g, b.hi[0] + g + 1)
+                ok = (xs >= 0) & (xs < n)
+                row = np.where(ok, glob[z, y, np.clip(xs, 0, n - 1)], np.nan)
+                fill = ~np.isnan(row)
+                want[kz, ky, fill] = row[fill]
+        assert bits_equal(got, want), first_diff(got, want)
