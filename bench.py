@@ -222,6 +222,19 @@ def run_ours(args) -> None:
         for _ in range(args.tune):
             run_loop(setup, prob.space, kern, tuner)
         params, best_s = tuner.best(setup)
+        # confirm the tuner's pick against its starting point on 20 launches each
+        # (single-sample medians early in a climb can crown a noisy winner)
+        def _avg_ms(p, n=20):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            prob.run(p)
+            a.record(stream)
+            for _ in range(n):
+                prob.run(p)
+            b.record(stream)
+            b.synchronize()
+            return a.elapsed_time(b) / n
+        if params != kern.default_params and _avg_ms(kern.default_params) <= _avg_ms(params):
+            params = kern.default_params
         if dist:   # every rank runs rank 0's choice
             obj = [params]
             dist.broadcast_object_list(obj, src=0)

@@ -198,6 +198,15 @@ SB_API int sb_copy_regions(const sb_copy_job *jobs, int32_t njobs, void *stream)
 SB_API int sb_copy_h2d(sb_array dst, const double *host, int32_t with_ghosts, void *stream);
 SB_API int sb_copy_d2h(double *host, sb_array src, int32_t with_ghosts, void *stream);
 
+/* The same for the z-plane range [p0, p1) of the host array's plane
+ * numbering (with ghosts: plane 0 is the first ghost plane); `host` is the
+ * base of the whole host array.  Lets a caller pipeline transfers with
+ * compute over z chunks. */
+SB_API int sb_copy_h2d_planes(sb_array dst, const double *host, int32_t with_ghosts, int32_t p0, int32_t p1,
+                              void *stream);
+SB_API int sb_copy_d2h_planes(double *host, sb_array src, int32_t with_ghosts, int32_t p0, int32_t p1,
+                              void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,17 +45,24 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) -> Path:
-    """Compile every CUDA source and link the shared library (no-op if fresh)."""
-    if not force and not ptxas_info and not _stale():
+def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False, variant: str | None = None,
+          defines: tuple[str, ...] = ()) -> Path:
+    """Compile every CUDA source and link the shared library (no-op if fresh).
+
+    ``variant``/``defines`` build an experimental copy
+    (libstencil_b200_<variant>.so, selected at run time with
+    STENCIL_B200_LIB) for A/B measurements; the product library is the
+    default build."""
+    lib = LIB if variant is None else PKG / f"libstencil_b200_{variant}.so"
+    if variant is None and not force and not ptxas_info and not _stale():
         return LIB
     cc = nvcc()
-    objdir = PKG / "build"
+    objdir = PKG / ("build" if variant is None else f"build_{variant}")
     objdir.mkdir(exist_ok=True)
     objs = []
     for src in SOURCES:
         obj = objdir / (src + ".o")
-        cmd = [cc, *NVCC_FLAGS, "-I", str(INCLUDE), "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [cc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", str(INCLUDE), "-c", str(CSRC / src), "-o", str(obj)]
         if ptxas_info:
             cmd += ["-Xptxas", "-v"]
         if verbose:
@@ -66,13 +73,13 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
         if ptxas_info and r.stderr:
             print(r.stderr, file=sys.stderr)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [cc, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-cudart", "static", *objs, "-o", str(tmp)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -27,7 +27,7 @@ SB_N_TERMS = 64
 EXPORTS = (
     "sb_abi_version", "sb_last_error", "sb_init", "sb_get_device_info", "sb_diff1d",
     "sb_lap7", "sb_d4_all", "sb_lap4_boxes", "sb_ghost_periodic", "sb_rk4_stage",
-    "sb_rhs24", "sb_copy_regions", "sb_copy_h2d", "sb_copy_d2h",
+    "sb_rhs24", "sb_copy_regions", "sb_copy_h2d", "sb_copy_d2h", "sb_copy_h2d_planes", "sb_copy_d2h_planes",
 )
 SB_MAX_COPY_JOBS = 64
 
@@ -98,6 +98,8 @@ def _declare(lib) -> None:
         "sb_copy_regions": ([C.POINTER(sb_copy_job), i32, vp], C.c_int),
         "sb_copy_h2d": ([sb_array, vp, i32, vp], C.c_int),
         "sb_copy_d2h": ([vp, sb_array, i32, vp], C.c_int),
+        "sb_copy_h2d_planes": ([sb_array, vp, i32, i32, i32, vp], C.c_int),
+        "sb_copy_d2h_planes": ([vp, sb_array, i32, i32, i32, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -110,7 +112,7 @@ def load(path: str | os.PathLike | None = None):
     global _lib
     with _lock:
         if _lib is None:
-            p = Path(path) if path else LIB_PATH
+            p = Path(path) if path else Path(os.environ.get("STENCIL_B200_LIB", LIB_PATH))
             if not p.exists():
                 raise DeviceError(f"{p} not built; run __graft_entry__.build() (no CPU fallback exists)")
             lib = C.CDLL(str(p))

@@ -82,8 +82,12 @@ class C2FourthOrder:
     def outputs(self) -> list[np.ndarray]:
         return [o.download() for o in self.outs]
 
-    # end-to-end through the C ABI with host buffers
-    def e2e_step(self, host_in_ptr: int, host_out_ptrs: list[int], params=None, stream=None) -> None:
+    # end-to-end through the public API with host buffers
+    def e2e_step(self, host_in_ptr: int, host_out_ptrs: list[int], params=None, stream=None,
+                 chunk: int | None = 32) -> None:
+        if chunk:
+            self.kernel.run_host(host_in_ptr, host_out_ptrs, params, chunk)
+            return
         self.src.upload_from_ptr(host_in_ptr, True, stream)
         self.run(params, stream)
         for o, p in zip(self.outs, host_out_ptrs):

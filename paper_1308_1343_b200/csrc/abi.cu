@@ -100,8 +100,11 @@ int make_tmap(CUtensorMap *m, const sb_array &a, int bx, int by, int bz) {
     cuuint64_t strides[2] = {(cuuint64_t)a.sy * 8, (cuuint64_t)a.sz * 8};
     cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
     cuuint32_t estr[3] = {1, 1, 1};
+#ifndef SB_TMA_L2_PROMOTION
+#define SB_TMA_L2_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
     CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, SB_TMA_L2_PROMOTION,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         char buf[160];
@@ -258,26 +261,40 @@ int sb_copy_regions(const sb_copy_job *jobs, int32_t njobs, void *stream) {
     return launch_copy_regions(jobs, njobs, as_stream(stream));
 }
 
+namespace {
+// Copy host planes [p0, p1) of a dense (z,y,x) host array to/from a grid.
+int copy_planes(bool h2d, double *host, const sb_array &a, int with_ghosts, int p0, int p1, cudaStream_t st) {
+    const int g = with_ghosts ? a.ghost : 0;
+    const size_t w = (size_t)(a.nx + 2 * g), rows_y = (size_t)(a.ny + 2 * g);
+    const int planes = a.nz + 2 * g;
+    if (p0 < 0 || p1 > planes || p0 > p1) return fail(SB_USAGE, "copy: plane range outside the array");
+    if (p0 == p1) return SB_OK;
+    double *d0 = a.origin - g - (int64_t)g * a.sy - (int64_t)g * a.sz + (int64_t)p0 * a.sz;
+    double *h0 = host + (size_t)p0 * rows_y * w;
+    const cudaMemcpyKind kind = h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+    if (a.sz == a.sy * (int64_t)(a.ny + 2 * a.ghost) && g == a.ghost) {
+        // planes are back to back: one 2-D copy of all rows of the range
+        const size_t rows = rows_y * (size_t)(p1 - p0);
+        return h2d ? check_cuda(cudaMemcpy2DAsync(d0, a.sy * 8, h0, w * 8, w * 8, rows, kind, st), "cudaMemcpy2DAsync h2d")
+                   : check_cuda(cudaMemcpy2DAsync(h0, w * 8, d0, a.sy * 8, w * 8, rows, kind, st), "cudaMemcpy2DAsync d2h");
+    }
+    for (int z = 0; z < p1 - p0; ++z) {
+        double *dz = d0 + (int64_t)z * a.sz;
+        double *hz = h0 + (size_t)z * rows_y * w;
+        int rc = h2d ? check_cuda(cudaMemcpy2DAsync(dz, a.sy * 8, hz, w * 8, w * 8, rows_y, kind, st), "cudaMemcpy2DAsync h2d")
+                     : check_cuda(cudaMemcpy2DAsync(hz, w * 8, dz, a.sy * 8, w * 8, rows_y, kind, st), "cudaMemcpy2DAsync d2h");
+        if (rc) return rc;
+    }
+    return SB_OK;
+}
+}  // namespace
+
 int sb_copy_h2d(sb_array dst, const double *host, int32_t with_ghosts, void *stream) {
     int rc = check_array(dst, 0, "copy_h2d");
     if (rc) return rc;
     if (!host) return fail(SB_USAGE, "copy_h2d: null host pointer");
     const int g = with_ghosts ? dst.ghost : 0;
-    const size_t w = (size_t)(dst.nx + 2 * g), rows_y = (size_t)(dst.ny + 2 * g), planes = (size_t)(dst.nz + 2 * g);
-    double *d0 = dst.origin - g - (int64_t)g * dst.sy - (int64_t)g * dst.sz;
-    if (dst.sz == dst.sy * (int64_t)(dst.ny + 2 * dst.ghost) && g == dst.ghost) {
-        // planes are back to back: one 2-D copy of all rows
-        return check_cuda(cudaMemcpy2DAsync(d0, dst.sy * 8, host, w * 8, w * 8, rows_y * planes,
-                                            cudaMemcpyHostToDevice, as_stream(stream)),
-                          "cudaMemcpy2DAsync h2d");
-    }
-    for (size_t z = 0; z < planes; ++z) {
-        rc = check_cuda(cudaMemcpy2DAsync(d0 + z * dst.sz, dst.sy * 8, host + z * rows_y * w, w * 8, w * 8, rows_y,
-                                          cudaMemcpyHostToDevice, as_stream(stream)),
-                        "cudaMemcpy2DAsync h2d");
-        if (rc) return rc;
-    }
-    return SB_OK;
+    return copy_planes(true, const_cast<double *>(host), dst, with_ghosts, 0, dst.nz + 2 * g, as_stream(stream));
 }
 
 int sb_copy_d2h(double *host, sb_array src, int32_t with_ghosts, void *stream) {
@@ -285,20 +302,21 @@ int sb_copy_d2h(double *host, sb_array src, int32_t with_ghosts, void *stream) {
     if (rc) return rc;
     if (!host) return fail(SB_USAGE, "copy_d2h: null host pointer");
     const int g = with_ghosts ? src.ghost : 0;
-    const size_t w = (size_t)(src.nx + 2 * g), rows_y = (size_t)(src.ny + 2 * g), planes = (size_t)(src.nz + 2 * g);
-    const double *s0 = src.origin - g - (int64_t)g * src.sy - (int64_t)g * src.sz;
-    if (src.sz == src.sy * (int64_t)(src.ny + 2 * src.ghost) && g == src.ghost) {
-        return check_cuda(cudaMemcpy2DAsync(host, w * 8, s0, src.sy * 8, w * 8, rows_y * planes,
-                                            cudaMemcpyDeviceToHost, as_stream(stream)),
-                          "cudaMemcpy2DAsync d2h");
-    }
-    for (size_t z = 0; z < planes; ++z) {
-        rc = check_cuda(cudaMemcpy2DAsync(host + z * rows_y * w, w * 8, s0 + z * src.sz, src.sy * 8, w * 8, rows_y,
-                                          cudaMemcpyDeviceToHost, as_stream(stream)),
-                        "cudaMemcpy2DAsync d2h");
-        if (rc) return rc;
-    }
-    return SB_OK;
+    return copy_planes(false, host, src, with_ghosts, 0, src.nz + 2 * g, as_stream(stream));
+}
+
+int sb_copy_h2d_planes(sb_array dst, const double *host, int32_t with_ghosts, int32_t p0, int32_t p1, void *stream) {
+    int rc = check_array(dst, 0, "copy_h2d_planes");
+    if (rc) return rc;
+    if (!host) return fail(SB_USAGE, "copy_h2d_planes: null host pointer");
+    return copy_planes(true, const_cast<double *>(host), dst, with_ghosts, p0, p1, as_stream(stream));
+}
+
+int sb_copy_d2h_planes(double *host, sb_array src, int32_t with_ghosts, int32_t p0, int32_t p1, void *stream) {
+    int rc = check_array(src, 0, "copy_d2h_planes");
+    if (rc) return rc;
+    if (!host) return fail(SB_USAGE, "copy_d2h_planes: null host pointer");
+    return copy_planes(false, host, src, with_ghosts, p0, p1, as_stream(stream));
 }
 
 }  // extern "C"

@@ -71,16 +71,21 @@ __host__ __device__ constexpr int n_pointwise(int mode) {
     return mode == D4_RK1 ? 1 : (mode == D4_RK23 || mode == D4_RK4) ? 5 : 0;
 }
 
-// Predicated streaming stores (no branches): pair / single lanes.
+// Predicated stores (no branches): pair / single lanes.  SB_STORE_HINT is
+// the cache operator of the output stream (default .cs: streaming,
+// evict-first — outputs are never re-read by the sweep).
+#ifndef SB_STORE_HINT
+#define SB_STORE_HINT ".cs"
+#endif
 __device__ __forceinline__ void st_v2(double *p, double a, double b, int pred) {
-    asm volatile(
-        "{\n.reg .pred q;\nsetp.ne.b32 q, %3, 0;\n@q st.global.cs.v2.f64 [%0], {%1, %2};\n}\n" ::"l"(p), "d"(a),
-        "d"(b), "r"(pred)
-        : "memory");
+    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %3, 0;\n@q st.global" SB_STORE_HINT
+                 ".v2.f64 [%0], {%1, %2};\n}\n" ::"l"(p),
+                 "d"(a), "d"(b), "r"(pred)
+                 : "memory");
 }
 __device__ __forceinline__ void st_1(double *p, double a, int pred) {
-    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.global.cs.f64 [%0], %1;\n}\n" ::"l"(p), "d"(a),
-                 "r"(pred)
+    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.global" SB_STORE_HINT ".f64 [%0], %1;\n}\n" ::"l"(p),
+                 "d"(a), "r"(pred)
                  : "memory");
 }
 

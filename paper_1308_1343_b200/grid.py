@@ -107,6 +107,15 @@ class DeviceGrid:
     def download_to_ptr(self, host_ptr: int, with_ghosts: bool = False, stream=None) -> None:
         _lib.call("sb_copy_d2h", int(host_ptr), self.abi(), int(bool(with_ghosts)), _stream_ptr(stream))
 
+    def upload_planes_from_ptr(self, host_ptr: int, with_ghosts: bool, p0: int, p1: int, stream=None) -> None:
+        """Asynchronous copy of host planes [p0, p1) (host plane numbering)."""
+        _lib.call("sb_copy_h2d_planes", self.abi(), int(host_ptr), int(bool(with_ghosts)), int(p0), int(p1),
+                  _stream_ptr(stream))
+
+    def download_planes_to_ptr(self, host_ptr: int, with_ghosts: bool, p0: int, p1: int, stream=None) -> None:
+        _lib.call("sb_copy_d2h_planes", int(host_ptr), self.abi(), int(bool(with_ghosts)), int(p0), int(p1),
+                  _stream_ptr(stream))
+
     def download(self, with_ghosts: bool = False, stream=None) -> np.ndarray:
         nx, ny, nz = self.extents
         g = self.ghost if with_ghosts else 0

@@ -113,6 +113,44 @@ class FourthOrderAll(DeviceKernel):
         _lib.call("sb_d4_all", self._out_abi, self.src.abi(), _local(space, self.src), _lib.d4_constants(self.k),
                   _lib.launch_of(params), stream_ptr(stream))
 
+    def run_host(self, host_in_ptr: int, host_out_ptrs: list[int], params: LaunchParams | None = None,
+                 chunk: int = 32) -> None:
+        """Whole-box sweep from/to host memory (pinned for overlap): the
+        ghosted input goes up, the box is swept and the ten outputs come back
+        z chunk by z chunk on three streams, so the uploads, the sweeps and the
+        downloads of different chunks overlap.  Ordered after the current
+        stream's prior work; the current stream waits for the last download."""
+        import torch
+        p = params or self.default_params
+        if not hasattr(self, "_streams"):
+            self._streams = tuple(torch.cuda.Stream() for _ in range(3))
+        up, cmp, down = self._streams
+        cur = torch.cuda.current_stream()
+        for s in self._streams:
+            s.wait_stream(cur)
+        cmp.wait_stream(down)     # outputs of a previous call are fully downloaded
+        up.wait_stream(cmp)       # and its sweeps are done reading the input
+        g = self.src.ghost
+        lo = self.src.lower
+        nx, ny, nz = self.src.extents
+        have = 0
+        for z0 in range(0, nz, chunk):
+            z1 = min(nz, z0 + chunk)
+            need = z1 + 2 * g                       # ghosted planes [0, z1 + 2g) feed planes < z1
+            self.src.upload_planes_from_ptr(host_in_ptr, True, have, need, up)
+            have = need
+            ev = torch.cuda.Event()
+            ev.record(up)
+            cmp.wait_event(ev)
+            space = IndexSpace((lo[0], lo[1], lo[2] + z0), (lo[0] + nx, lo[1] + ny, lo[2] + z1))
+            self.launch(space, p, cmp)
+            ev = torch.cuda.Event()
+            ev.record(cmp)
+            down.wait_event(ev)
+            for o, ptr in zip(self.outs, host_out_ptrs):
+                o.download_planes_to_ptr(ptr, False, z0, z1, down)
+        cur.wait_stream(down)
+
 
 class Laplacian4(DeviceKernel):
     """K3 — 4th-order Laplacian of one box; see :class:`LevelLaplacian4` for levels."""

@@ -391,3 +391,26 @@ def test_level_ghost_sync_matches_global_field():
                 fill = ~np.isnan(row)
                 want[kz, ky, fill] = row[fill]
         assert bits_equal(got, want), first_diff(got, want)
+
+
+@pytest.mark.parametrize("chunk", [None, 16, 100])
+def test_c2_host_pipeline_matches_device_run(chunk):
+    """run_host (chunked H2D / sweep / D2H on three streams) returns the same
+    bits as the resident sweep, and uploads the whole input."""
+    import torch
+    from paper_1308_1343_b200.configs import C2FourthOrder
+    n = 72
+    p = C2FourthOrder(n=n, seed=31).setup()
+    p.run()
+    want = p.outputs()
+    p.src.fill_(0.0)
+    for o in p.outs:
+        o.fill_(0.0)
+    h_in = torch.from_numpy(p.host_u).pin_memory()
+    h_out = [torch.empty((n, n, n), dtype=torch.float64).pin_memory() for _ in range(10)]
+    for _ in range(2):
+        p.e2e_step(h_in.data_ptr(), [t.data_ptr() for t in h_out], chunk=chunk)
+    torch.cuda.synchronize()
+    for w, h in zip(want, h_out):
+        assert bits_equal(h.numpy(), w)
+    assert bits_equal(p.src.download(with_ghosts=True), p.host_u)
