@@ -207,6 +207,14 @@ SB_API int sb_copy_h2d_planes(sb_array dst, const double *host, int32_t with_gho
 SB_API int sb_copy_d2h_planes(double *host, sb_array src, int32_t with_ghosts, int32_t p0, int32_t p1,
                               void *stream);
 
+/* Upload host planes [p0, p1) through a dense device staging buffer (at
+ * least as large as the whole dense host array): one linear H2D copy at
+ * full PCIe speed, then an on-device unpack into the padded rows of `dst`.
+ * (A pitched 2-D H2D copy runs at a third of the link rate and does not
+ * overlap D2H traffic.) */
+SB_API int sb_copy_h2d_planes_staged(sb_array dst, const double *host, double *staging, int32_t with_ghosts,
+                                     int32_t p0, int32_t p1, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,6 +28,7 @@ EXPORTS = (
     "sb_abi_version", "sb_last_error", "sb_init", "sb_get_device_info", "sb_diff1d",
     "sb_lap7", "sb_d4_all", "sb_lap4_boxes", "sb_ghost_periodic", "sb_rk4_stage",
     "sb_rhs24", "sb_copy_regions", "sb_copy_h2d", "sb_copy_d2h", "sb_copy_h2d_planes", "sb_copy_d2h_planes",
+    "sb_copy_h2d_planes_staged",
 )
 SB_MAX_COPY_JOBS = 64
 
@@ -100,6 +101,7 @@ def _declare(lib) -> None:
         "sb_copy_d2h": ([vp, sb_array, i32, vp], C.c_int),
         "sb_copy_h2d_planes": ([sb_array, vp, i32, i32, i32, vp], C.c_int),
         "sb_copy_d2h_planes": ([vp, sb_array, i32, i32, i32, vp], C.c_int),
+        "sb_copy_h2d_planes_staged": ([sb_array, vp, vp, i32, i32, i32, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -273,8 +273,11 @@ int copy_planes(bool h2d, double *host, const sb_array &a, int with_ghosts, int 
     double *h0 = host + (size_t)p0 * rows_y * w;
     const cudaMemcpyKind kind = h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
     if (a.sz == a.sy * (int64_t)(a.ny + 2 * a.ghost) && g == a.ghost) {
-        // planes are back to back: one 2-D copy of all rows of the range
+        // planes are back to back: one copy of all rows of the range
         const size_t rows = rows_y * (size_t)(p1 - p0);
+        if ((size_t)a.sy == w)   // dense rows too: a plain 1-D copy (faster than 2-D over PCIe)
+            return h2d ? check_cuda(cudaMemcpyAsync(d0, h0, rows * w * 8, kind, st), "cudaMemcpyAsync h2d")
+                       : check_cuda(cudaMemcpyAsync(h0, d0, rows * w * 8, kind, st), "cudaMemcpyAsync d2h");
         return h2d ? check_cuda(cudaMemcpy2DAsync(d0, a.sy * 8, h0, w * 8, w * 8, rows, kind, st), "cudaMemcpy2DAsync h2d")
                    : check_cuda(cudaMemcpy2DAsync(h0, w * 8, d0, a.sy * 8, w * 8, rows, kind, st), "cudaMemcpy2DAsync d2h");
     }
@@ -317,6 +320,24 @@ int sb_copy_d2h_planes(double *host, sb_array src, int32_t with_ghosts, int32_t 
     if (rc) return rc;
     if (!host) return fail(SB_USAGE, "copy_d2h_planes: null host pointer");
     return copy_planes(false, host, src, with_ghosts, p0, p1, as_stream(stream));
+}
+
+int sb_copy_h2d_planes_staged(sb_array dst, const double *host, double *staging, int32_t with_ghosts, int32_t p0,
+                              int32_t p1, void *stream) {
+    int rc = check_array(dst, 0, "copy_h2d_planes_staged");
+    if (rc) return rc;
+    if (!host || !staging) return fail(SB_USAGE, "copy_h2d_planes_staged: null pointer");
+    const int g = with_ghosts ? dst.ghost : 0;
+    const size_t w = (size_t)(dst.nx + 2 * g), rows_y = (size_t)(dst.ny + 2 * g);
+    const int planes = dst.nz + 2 * g;
+    if (p0 < 0 || p1 > planes || p0 > p1) return fail(SB_USAGE, "copy_h2d_planes_staged: plane range outside the array");
+    if (p0 == p1) return SB_OK;
+    const size_t off = (size_t)p0 * rows_y * w, n = (size_t)(p1 - p0) * rows_y * w;
+    rc = check_cuda(cudaMemcpyAsync(staging + off, host + off, n * 8, cudaMemcpyHostToDevice, as_stream(stream)),
+                    "cudaMemcpyAsync h2d (staged)");
+    if (rc) return rc;
+    double *d0 = dst.origin - g - (int64_t)g * dst.sy - (int64_t)g * dst.sz + (int64_t)p0 * dst.sz;
+    return launch_unpack_rows(d0, dst.sy, dst.sz, (int)w, (int)rows_y, staging + off, (long long)n, as_stream(stream));
 }
 
 }  // extern "C"

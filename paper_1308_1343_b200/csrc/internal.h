@@ -38,6 +38,8 @@ int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, 
 int launch_ghost_periodic(const sb_array &a, cudaStream_t st);
 
 int launch_copy_regions(const sb_copy_job *jobs, int njobs, cudaStream_t st);
+int launch_unpack_rows(double *dst, long long sy, long long sz, int w, int rows_y, const double *src, long long n,
+                       cudaStream_t st);
 
 int launch_rhs24(const sb_array *in, const sb_array *out, const sb_space &sp, const sb_d4_constants &k,
                  const sb_poly &poly, const sb_launch &p, cudaStream_t st);

@@ -49,7 +49,29 @@ bool inside(const sb_array &a, const int lo[3], const int ext[3], int halo) {
     return true;
 }
 
+// Dense rows (w doubles each, rows_y rows per plane) -> padded rows of a grid.
+__global__ void unpack_rows_kernel(double *dst, long long sy, long long sz, int w, int rows_y, const double *src,
+                                   long long n) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+        const long long row = t / w;
+        const int col = (int)(t - row * w);
+        const int y = (int)(row % rows_y);
+        const long long z = row / rows_y;
+        dst[col + y * sy + z * sz] = src[t];
+    }
+}
+
 }  // namespace
+
+int launch_unpack_rows(double *dst, long long sy, long long sz, int w, int rows_y, const double *src, long long n,
+                       cudaStream_t st) {
+    if (n <= 0) return SB_OK;
+    const int threads = 256;
+    long long blocks = (n + threads - 1) / threads;
+    if (blocks > 148LL * 32) blocks = 148LL * 32;
+    unpack_rows_kernel<<<(unsigned)blocks, threads, 0, st>>>(dst, sy, sz, w, rows_y, src, n);
+    return check_cuda(cudaGetLastError(), "unpack_rows_kernel launch");
+}
 
 int launch_copy_regions(const sb_copy_job *jobs, int njobs, cudaStream_t st) {
     if (njobs == 0) return SB_OK;

@@ -112,6 +112,19 @@ class DeviceGrid:
         _lib.call("sb_copy_h2d_planes", self.abi(), int(host_ptr), int(bool(with_ghosts)), int(p0), int(p1),
                   _stream_ptr(stream))
 
+    def upload_planes_staged(self, host_ptr: int, staging, with_ghosts: bool, p0: int, p1: int,
+                             stream=None) -> None:
+        """Host planes [p0, p1) via a dense device staging tensor (linear H2D at
+        full link speed + on-device unpack into the padded rows)."""
+        _lib.call("sb_copy_h2d_planes_staged", self.abi(), int(host_ptr), int(staging.data_ptr()),
+                  int(bool(with_ghosts)), int(p0), int(p1), _stream_ptr(stream))
+
+    def staging_buffer(self, with_ghosts: bool = True):
+        import torch
+        nx, ny, nz = self.extents
+        g = self.ghost if with_ghosts else 0
+        return torch.empty((nz + 2 * g) * (ny + 2 * g) * (nx + 2 * g), dtype=torch.float64, device=self.device)
+
     def download_planes_to_ptr(self, host_ptr: int, with_ghosts: bool, p0: int, p1: int, stream=None) -> None:
         _lib.call("sb_copy_d2h_planes", int(host_ptr), self.abi(), int(bool(with_ghosts)), int(p0), int(p1),
                   _stream_ptr(stream))

@@ -124,6 +124,7 @@ class FourthOrderAll(DeviceKernel):
         p = params or self.default_params
         if not hasattr(self, "_streams"):
             self._streams = tuple(torch.cuda.Stream() for _ in range(3))
+            self._staging = self.src.staging_buffer(True)
         up, cmp, down = self._streams
         cur = torch.cuda.current_stream()
         for s in self._streams:
@@ -137,7 +138,7 @@ class FourthOrderAll(DeviceKernel):
         for z0 in range(0, nz, chunk):
             z1 = min(nz, z0 + chunk)
             need = z1 + 2 * g                       # ghosted planes [0, z1 + 2g) feed planes < z1
-            self.src.upload_planes_from_ptr(host_in_ptr, True, have, need, up)
+            self.src.upload_planes_staged(host_in_ptr, self._staging, True, have, need, up)
             have = need
             ev = torch.cuda.Event()
             ev.record(up)
