@@ -79,6 +79,13 @@ struct Rings {
     double u[5], rx[5], ry[5];
 };
 
+// Physical row of logical row r (0..7) of an 8-wide rx plane: parity pattern
+// 0,0,1,1,0,0,1,1 keeps rows r and r+2 in different 64-byte bank halves.
+__device__ __forceinline__ int rxrow(int r) {
+    constexpr unsigned kPerm = 0u | (2u << 3) | (1u << 6) | (3u << 9) | (4u << 12) | (6u << 15) | (5u << 18) | (7u << 21);
+    return (kPerm >> (3 * r)) & 7;
+}
+
 // thread 0: all 24 field planes of stream plane j into stage j % NSTAGE
 __device__ __forceinline__ void issue(const Rhs24Params &P, const Ctx &c, int j) {
     const int s = j % NSTAGE;
@@ -106,11 +113,12 @@ __device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c,
         rg.rx[R] = d1u(row[0], row[1], row[3], row[4]);
         rg.ry[R] = d1u(col[0], col[HXc], col[3 * HXc], col[4 * HXc]);
         double *rxs = c.rxb + ((i % 3) * NV + v) * (HYc * TXc);
-        rxs[(c.cy + 2) * TXc + c.cx] = rg.rx[R];
-        const int h = c.lane >> 3, hc = c.lane & 7;      // lanes double as 4 halo rows x 8 columns
-        const int hr = h < 2 ? h : TYc + h;
+        rxs[rxrow(c.cy + 2) * TXc + c.cx] = rg.rx[R];
+        // lanes double as the 4 halo rows x 8 columns; half-warps take rows {0, 6} and {1, 7}
+        const int h = c.lane >> 3, hc = c.lane & 7;
+        const int hr = (h & 1) ? 6 + (h >> 1) : (h >> 1);
         const double *hrow = pl + hr * HXc + hc;
-        rxs[hr * TXc + hc] = d1u(hrow[0], hrow[1], hrow[3], hrow[4]);
+        rxs[rxrow(hr) * TXc + hc] = d1u(hrow[0], hrow[1], hrow[3], hrow[4]);
     }
 
     // ---- phase A, completed plane zc = z-2: the ten slots ----
@@ -132,8 +140,8 @@ __device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c,
         o[4 * NCOL] = d2(row[0], row[1], uc, row[3], row[4], P.k2);
         o[5 * NCOL] = d2(col[0], col[HXc], uc, col[3 * HXc], col[4 * HXc], P.k2);
         o[6 * NCOL] = d2(rg.u[K0], rg.u[K1], uc, rg.u[K3], rg.u[K4], P.k2);
-        o[7 * NCOL] = mul(d1u(rxs[(c.cy + 0) * TXc], rxs[(c.cy + 1) * TXc], rxs[(c.cy + 3) * TXc],
-                              rxs[(c.cy + 4) * TXc]),
+        o[7 * NCOL] = mul(d1u(rxs[rxrow(c.cy + 0) * TXc], rxs[rxrow(c.cy + 1) * TXc], rxs[rxrow(c.cy + 3) * TXc],
+                              rxs[rxrow(c.cy + 4) * TXc]),
                           P.k11);
         o[8 * NCOL] = mul(d1u(rg.rx[K0], rg.rx[K1], rg.rx[K3], rg.rx[K4]), P.k11);
         o[9 * NCOL] = mul(d1u(rg.ry[K0], rg.ry[K1], rg.ry[K3], rg.ry[K4]), P.k11);
@@ -152,12 +160,20 @@ __device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c,
         const Term *tt = c.terms + c.warp * NT;
         const char *vb = reinterpret_cast<const char *>(c.vals + c.lane);
         auto V = [vb](uint32_t off) { return *reinterpret_cast<const double *>(vb + off); };
-        Term t0 = tt[0];
-        double acc = mul(mul(t0.c, V(t0.pq & 0xffffu)), V(t0.pq >> 16));
+        // one 16-byte broadcast load per term: (c, pq | pad)
+        auto T = [tt](int k, double &cf, uint32_t &pq) {
+            const double2 raw = *reinterpret_cast<const double2 *>(tt + k);
+            cf = raw.x;
+            pq = (uint32_t)__double_as_longlong(raw.y);
+        };
+        double cf;
+        uint32_t pq;
+        T(0, cf, pq);
+        double acc = mul(mul(cf, V(pq & 0xffffu)), V(pq >> 16));
 #pragma unroll 16
         for (int k = 1; k < NT; ++k) {
-            const Term tk = tt[k];
-            acc = add(acc, mul(mul(tk.c, V(tk.pq & 0xffffu)), V(tk.pq >> 16)));
+            T(k, cf, pq);
+            acc = add(acc, mul(mul(cf, V(pq & 0xffffu)), V(pq >> 16)));
         }
         if (c.active) {
             const int zc = c.Z0 - 4 + i;
@@ -180,8 +196,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) rhs24_kernel(const __grid_constan
     c.tid = threadIdx.x;
     c.warp = c.tid >> 5;
     c.lane = c.tid & 31;
+    // lanes 0-7 -> row 0, 8-15 -> row 2, 16-23 -> row 1, 24-31 -> row 3: each
+    // half-warp reads two rows 24 doubles apart in the 12-wide staged planes,
+    // i.e. disjoint bank halves (rows 12 apart would share 4 bank pairs)
     c.cx = c.lane & 7;
-    c.cy = c.lane >> 3;
+    c.cy = ((c.lane >> 3) & 1) * 2 + (c.lane >> 4);
     int t = blockIdx.x;
     const int bx = t % P.ntx;
     t /= P.ntx;
