@@ -180,27 +180,36 @@ __device__ __forceinline__ void issue_plane(const Ctx &c, const D4Params &P, con
     }
 }
 
-// Store v at (x+j, y, z) and, for a periodic box, at every ghost point whose
-// periodic image it is (fused ghost refill; exact copies).
+// Store-side periodic ghost refresh: also write v at every ghost point that is
+// a periodic image of interior point (x+j, y, z).  Per axis the images are
+// +n (when the point is within g of the low face) and -n (within g of the
+// high face) — both when 2g > n.  Exact copies.
+__device__ __forceinline__ int images(int c, int n, int g, int (&o)[3]) {
+    int k = 0;
+    o[k++] = 0;
+    if (c < g) o[k++] = n;
+    if (c >= n - g) o[k++] = -n;
+    return k;
+}
+
 template <int NP>
 __device__ __forceinline__ void store_periodic(double *base, long long sy, long long sz, const D4Params &P, int x,
                                                int y, int z, const double (&v)[NP], const Lanes<NP> &L) {
     const int g = P.pghost;
-    const int ny = P.per[1], nz = P.per[2], nx = P.per[0];
-    const int oy = y < g ? ny : (y >= ny - g ? -ny : 0);
-    const int oz = z < g ? nz : (z >= nz - g ? -nz : 0);
+    if (x >= g && x + NP <= P.per[0] - g && y >= g && y < P.per[1] - g && z >= g && z < P.per[2] - g) return;
+    int oy[3], oz[3];
+    const int ky = images(y, P.per[1], g, oy), kz = images(z, P.per[2], g, oz);
 #pragma unroll
     for (int j = 0; j < NP; ++j) {
         if (!L.m[j]) continue;
-        const int xs = x + j;
-        const int ox = xs < g ? nx : (xs >= nx - g ? -nx : 0);
-        if ((ox | oy | oz) == 0) continue;
-        double *p0 = base + xs + (long long)y * sy + (long long)z * sz;
-        for (int m = 1; m < 8; ++m) {
-            const int dx = (m & 1) ? ox : 0, dy = (m & 2) ? oy : 0, dz = (m & 4) ? oz : 0;
-            if (((m & 1) && !ox) || ((m & 2) && !oy) || ((m & 4) && !oz)) continue;
-            p0[dx + (long long)dy * sy + (long long)dz * sz] = v[j];
-        }
+        int ox[3];
+        const int kx = images(x + j, P.per[0], g, ox);
+        if (kx * ky * kz == 1) continue;
+        double *p0 = base + (x + j) + (long long)y * sy + (long long)z * sz;
+        for (int a = 0; a < kz; ++a)
+            for (int b = 0; b < ky; ++b)
+                for (int d = 0; d < kx; ++d)
+                    if (a | b | d) p0[ox[d] + (long long)oy[b] * sy + (long long)oz[a] * sz] = v[j];
     }
 }
 

@@ -1,0 +1,117 @@
+"""Edge cases through the C ABI: ragged and odd extents, thin boxes, offset
+boxes, empty spaces, single points — every kernel bit-exact vs the oracle."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1308_1343_b200 import _build, inputs
+from paper_1308_1343_b200.tuner import LaunchParams
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    _build.build()
+
+
+def same(a, b):
+    return a.shape == b.shape and np.ascontiguousarray(a).tobytes() == np.ascontiguousarray(b).tobytes()
+
+
+def d4_setup(ext, g=2, seed=0, lower=(0, 0, 0)):
+    from paper_1308_1343_b200.grid import DeviceGrid
+    from paper_1308_1343_b200.kernels import FourthOrderAll
+    nx, ny, nz = ext
+    rng = np.random.default_rng(seed)
+    u = rng.uniform(-1, 1, (nz + 2 * g, ny + 2 * g, nx + 2 * g))
+    k = inputs.D4Constants.for_spacing(1.0 / 17)
+    src = DeviceGrid(ext, g, lower=lower)
+    src.upload(u)
+    outs = [DeviceGrid(ext, 0, lower=lower).fill_(0.25) for _ in range(10)]
+    return u, k, src, outs, FourthOrderAll(outs, src, k)
+
+
+@pytest.mark.parametrize("ext", [(37, 23, 11), (1, 1, 1), (5, 3, 1), (64, 1, 9), (130, 7, 3)])
+@pytest.mark.parametrize("params", [(32, 4, 4, 2), (64, 2, 7, 1), (128, 1, 64, 2)])
+def test_d4_all_ragged(ext, params):
+    from paper_1308_1343_b200.traverse import IndexSpace
+    u, k, src, outs, kern = d4_setup(ext, seed=sum(ext))
+    nx, ny, nz = ext
+    kern.launch(IndexSpace((0, 0, 0), ext), LaunchParams(*params))
+    want = [np.empty((nz, ny, nx)) for _ in range(10)]
+    oracle.d4_all(want, u, 2, (0, nx, 0, ny, 0, nz), k)
+    for i in range(10):
+        assert same(outs[i].download(), want[i]), (ext, params, i)
+
+
+def test_empty_space_writes_nothing():
+    from paper_1308_1343_b200.traverse import IndexSpace
+    u, k, src, outs, kern = d4_setup((16, 16, 16))
+    kern.launch(IndexSpace((3, 3, 3), (3, 9, 9)), LaunchParams(32, 4, 4, 2))
+    for o in outs:
+        assert (o.download() == 0.25).all()
+
+
+def test_offset_box_level_coordinates():
+    """A box whose lower corner is (100, -7, 33) in level coordinates."""
+    from paper_1308_1343_b200.traverse import IndexSpace
+    lower = (100, -7, 33)
+    ext = (20, 12, 9)
+    u, k, src, outs, kern = d4_setup(ext, seed=4, lower=lower)
+    sub = IndexSpace((103, -5, 34), (119, 4, 41))      # local [3,19) x [2,11) x [1,8)
+    kern.launch(sub, LaunchParams(32, 4, 3, 2))
+    want = [np.full((9, 12, 20), 0.25) for _ in range(10)]
+    oracle.d4_all(want, u, 2, (3, 19, 2, 11, 1, 8), k)
+    for i in range(10):
+        assert same(outs[i].download(), want[i]), i
+
+
+@pytest.mark.parametrize("n", [1, 3, 30])
+def test_rk4_small_and_ragged_periodic(n):
+    from paper_1308_1343_b200.configs import C3WaveRK4
+    g = 2
+    if n < g:
+        pytest.skip("periodic ghost width must not exceed the extent")
+    p = C3WaveRK4(n=n, seed=n).setup()
+    p.run(LaunchParams(32, 4, 5, 1))
+    wphi, wpi = oracle.rk4_step(p.host_phi, p.host_pi, g, p.c)
+    assert same(p.phi_with_ghosts(), wphi)
+    I = (slice(g, g + n),) * 3
+    assert same(p.outputs()[1], wpi[I])
+
+
+@pytest.mark.parametrize("n,zc", [(13, 5), (9, 192), (2, 1)])
+def test_rhs24_ragged(n, zc):
+    from paper_1308_1343_b200.configs import C5Rhs24
+    p = C5Rhs24(n=n, seed=n + 100).setup()
+    p.run(LaunchParams(32, 24, zc, 1))
+    want = [np.empty((n, n, n)) for _ in range(24)]
+    oracle.rhs24(want, p.host_u, 2, (0, n, 0, n, 0, n), p.k, p.poly)
+    for o, got in enumerate(p.outputs()):
+        assert same(got, want[o]), o
+
+
+@pytest.mark.parametrize("n", [1, 2, 7])
+def test_lap7_tiny(n):
+    from paper_1308_1343_b200.configs import C1Laplacian7
+    p = C1Laplacian7(n=n, seed=n).setup()
+    p.run()
+    u = p.host_u
+    ref = u.copy()
+    oracle.lap7_rows(ref, u, 1, n + 1, 1, n + 1, 1, n + 1, p.c0, p.c1)
+    assert same(p.outputs()[0], ref[1:-1, 1:-1, 1:-1])
+
+
+def test_level_with_many_boxes_chunks_launches():
+    """More boxes than SB_MAX_BOXES: the level kernel splits into launches."""
+    from paper_1308_1343_b200.configs import C4Level
+    from paper_1308_1343_b200.level import Box
+    boxes = [Box((8 * i, 0, 0), (8 * i + 6, 5, 4 + i % 3)) for i in range(11)]
+    p = C4Level(n=96, seed=8, boxes=boxes).setup()
+    p.run(LaunchParams(32, 4, 2, 2))
+    for b, u, got in zip(p.boxes, p.host_u, p.outputs()):
+        nx, ny, nz = b.extents
+        want = np.empty((nz, ny, nx))
+        oracle.lap4(want, u, 2, (0, nx, 0, ny, 0, nz), p.k.k2)
+        assert same(got, want), b
