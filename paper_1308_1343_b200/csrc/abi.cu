@@ -229,6 +229,13 @@ int sb_rk4_stage(int32_t stage, const sb_rk4_fields *f, sb_space space, sb_rk4_c
         job.g[4] = f->pi0;
         mode = D4_RK1;
         ca = c.half_dt;
+    } else if (stage == 2) {
+        job.g[4] = f->pi_s;
+        job.g[5] = f->phi0;
+        job.g[6] = f->pi0;
+        job.g[7] = f->acc_pi;
+        mode = D4_RK2;
+        ca = c.half_dt;
     } else {
         job.g[4] = f->pi_s;
         job.g[5] = f->phi0;
@@ -236,7 +243,7 @@ int sb_rk4_stage(int32_t stage, const sb_rk4_fields *f, sb_space space, sb_rk4_c
         job.g[7] = f->acc_phi;
         job.g[8] = f->acc_pi;
         mode = stage == 4 ? D4_RK4 : D4_RK23;
-        ca = stage == 2 ? c.half_dt : (stage == 3 ? c.dt : c.dt6);
+        ca = stage == 3 ? c.dt : c.dt6;
     }
     return launch_d4(mode, &job, 1, c.lap, ca, 0.0, p, as_stream(stream));
 }

@@ -68,7 +68,7 @@ struct D4Params {
 };
 
 __host__ __device__ constexpr int n_pointwise(int mode) {
-    return mode == D4_RK1 ? 1 : (mode == D4_RK23 || mode == D4_RK4) ? 5 : 0;
+    return mode == D4_RK1 ? 1 : mode == D4_RK2 ? 4 : (mode == D4_RK23 || mode == D4_RK4) ? 5 : 0;
 }
 
 // Predicated stores (no branches): pair / single lanes.  SB_STORE_HINT is
@@ -185,11 +185,23 @@ __device__ __forceinline__ void issue_plane(const Ctx &c, const D4Params &P, con
 // +n (when the point is within g of the low face) and -n (within g of the
 // high face) — both when 2g > n.  Exact copies.
 __device__ __forceinline__ int images(int c, int n, int g, int (&o)[3]) {
-    int k = 0;
-    o[k++] = 0;
-    if (c < g) o[k++] = n;
-    if (c >= n - g) o[k++] = -n;
-    return k;
+    const bool lo = c < g, hi = c >= n - g;
+    o[0] = 0;
+    o[1] = lo ? n : -n;
+    o[2] = -n;
+    return 1 + (int)lo + (int)hi;
+}
+
+// Rare path, kept out of line so the unrolled plane loop stays small.
+__device__ __noinline__ void store_images(double *base, long long sy, long long sz, int nx, int ny, int nz, int g,
+                                          int x, int y, int z, double v) {
+    int ox[3], oy[3], oz[3];
+    const int kx = images(x, nx, g, ox), ky = images(y, ny, g, oy), kz = images(z, nz, g, oz);
+    double *p0 = base + x + (long long)y * sy + (long long)z * sz;
+    for (int a = 0; a < kz; ++a)
+        for (int b = 0; b < ky; ++b)
+            for (int d = 0; d < kx; ++d)
+                if (a | b | d) p0[ox[d] + (long long)oy[b] * sy + (long long)oz[a] * sz] = v;
 }
 
 template <int NP>
@@ -197,20 +209,9 @@ __device__ __forceinline__ void store_periodic(double *base, long long sy, long 
                                                int y, int z, const double (&v)[NP], const Lanes<NP> &L) {
     const int g = P.pghost;
     if (x >= g && x + NP <= P.per[0] - g && y >= g && y < P.per[1] - g && z >= g && z < P.per[2] - g) return;
-    int oy[3], oz[3];
-    const int ky = images(y, P.per[1], g, oy), kz = images(z, P.per[2], g, oz);
 #pragma unroll
-    for (int j = 0; j < NP; ++j) {
-        if (!L.m[j]) continue;
-        int ox[3];
-        const int kx = images(x + j, P.per[0], g, ox);
-        if (kx * ky * kz == 1) continue;
-        double *p0 = base + (x + j) + (long long)y * sy + (long long)z * sz;
-        for (int a = 0; a < kz; ++a)
-            for (int b = 0; b < ky; ++b)
-                for (int d = 0; d < kx; ++d)
-                    if (a | b | d) p0[ox[d] + (long long)oy[b] * sy + (long long)oz[a] * sz] = v[j];
-    }
+    for (int j = 0; j < NP; ++j)
+        if (L.m[j]) store_images(base, sy, sz, P.per[0], P.per[1], P.per[2], g, x + j, y, z, v[j]);
 }
 
 template <int MODE, int TX, int NP, int R>
@@ -336,7 +337,8 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
     } else if constexpr (MODE == D4_LAP4) {
         store<NP>(B.g[0] + offc, lap, L);
     } else if constexpr (MODE == D4_RK1) {
-        // k1 = (pi0, L(phi0)); phi2 = phi0 + (dt/2) pi0; pi2 = pi0 + (dt/2) L; acc = k1
+        // k1 = (pi0, L(phi0)); phi2 = phi0 + (dt/2) pi0; pi2 = pi0 + (dt/2) L;
+        // acc_pi = L (acc_phi = k1_phi = pi0 is formed by stage 2 from pi0 itself)
         const double cc = P.ca;
         double fo[NP], po[NP];
 #pragma unroll
@@ -347,8 +349,23 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
         store<NP>(B.g[0] + offc, fo, L);
         if (P.per[0]) store_periodic<NP>(B.g[0], B.sy, B.sz, P, c.X0 + NP * c.cx, c.Y0 + c.ry, zc, fo, L);
         store<NP>(B.g[1] + offc, po, L);
-        store<NP>(B.g[2] + offc, pw[0], L);
         store<NP>(B.g[3] + offc, lap, L);
+    } else if constexpr (MODE == D4_RK2) {
+        // pw: 0 pi_s, 1 phi0, 2 pi0, 3 acc_pi;  acc_phi = pi0 + 2 pi_s  (= k1 + 2 k2)
+        const double cc = P.ca;
+        double o0[NP], o1[NP], o2[NP], o3[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            o0[j] = add(pw[1][j], mul(cc, pw[0][j]));
+            o1[j] = add(pw[2][j], mul(cc, lap[j]));
+            o2[j] = add(pw[2][j], mul(2.0, pw[0][j]));
+            o3[j] = add(pw[3][j], mul(2.0, lap[j]));
+        }
+        store<NP>(B.g[0] + offc, o0, L);
+        if (P.per[0]) store_periodic<NP>(B.g[0], B.sy, B.sz, P, c.X0 + NP * c.cx, c.Y0 + c.ry, zc, o0, L);
+        store<NP>(B.g[1] + offc, o1, L);
+        store<NP>(B.g[2] + offc, o2, L);
+        store<NP>(B.g[3] + offc, o3, L);
     } else {
         // pw: 0 pi_s, 1 phi0, 2 pi0, 3 acc_phi, 4 acc_pi
         const double cc = P.ca;
@@ -510,7 +527,7 @@ int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, 
                               "within the mode's limit (256 for paired d4_all / RK stages, else 512)");
     if (TY + 4 > 256) return fail(SB_USAGE, "tile_y + 4 exceeds the TMA box limit of 256");
     if (smem_bytes(mode, TX, TY) > 227 * 1024) return fail(SB_RESOURCE, "tile needs more than 227 KB of shared memory");
-    const int nused = mode == D4_ALL10 ? 10 : mode == D4_LAP4 ? 1 : mode == D4_RK1 ? 5 : 9;
+    const int nused = mode == D4_ALL10 ? 10 : mode == D4_LAP4 ? 1 : mode == D4_RK1 ? 5 : mode == D4_RK2 ? 8 : 9;
 
     D4Params P;
     memset(&P, 0, sizeof(P));
@@ -585,6 +602,7 @@ int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, 
         case D4_RK1: return launch_np<D4_RK1>(P, TX, NP, nb, st);
         case D4_RK23: return launch_np<D4_RK23>(P, TX, NP, nb, st);
         case D4_RK4: return launch_np<D4_RK4>(P, TX, NP, nb, st);
+        case D4_RK2: return launch_np<D4_RK2>(P, TX, NP, nb, st);
         default: return fail(SB_USAGE, "unknown d4 mode");
     }
 }

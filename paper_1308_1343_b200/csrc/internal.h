@@ -24,7 +24,9 @@ int launch_lap7(const sb_array &dst, const sb_array &src, const sb_space &sp, do
                 const sb_launch &p, cudaStream_t st);
 int launch_diff1d(int kind, double *dst, const double *src, int n, cudaStream_t st);
 
-enum D4Mode { D4_ALL10 = 0, D4_LAP4 = 1, D4_RK1 = 2, D4_RK23 = 3, D4_RK4 = 4 };
+// RK stages: RK1 = stage 1, RK2 = stage 2 (acc_phi = pi0 + 2 pi_s: stage 1 never
+// materialises acc_phi = pi0), RK23 = stage 3, RK4 = stage 4.
+enum D4Mode { D4_ALL10 = 0, D4_LAP4 = 1, D4_RK1 = 2, D4_RK23 = 3, D4_RK4 = 4, D4_RK2 = 5 };
 
 struct D4Job {
     sb_array src;         // stencil input (ghost >= 2)

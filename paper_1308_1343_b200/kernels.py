@@ -289,7 +289,7 @@ class WaveRK4:
         self.phi_a, self.pi_a, self.phi_b, self.pi_b = mk(), mk(), mk(), mk()
         self.acc_phi, self.acc_pi = mk(), mk()
         # best of the sweep at 384^3 (profiles/r01/v3_sweep_c3_tma_pointwise_fused_ghosts.jsonl)
-        self.params = LaunchParams(64, 4, 16, 1)
+        self.params = LaunchParams(64, 4, 16, 1)   # v4 A/B: profiles/r01/v4_c3_rk2_ab.log
 
     def launch_space(self) -> LaunchSpace:
         return RK4_SPACE
