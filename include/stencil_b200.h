@@ -184,6 +184,26 @@ SB_API int sb_ghost_periodic(sb_array a, void *stream);
 SB_API int sb_rk4_stage(int32_t stage, const sb_rk4_fields *f, sb_space space,
                  sb_rk4_constants c, sb_launch p, void *stream);
 
+/* F4 — z-slab decomposition of one periodic box over several GPUs (or
+ * several slabs of one GPU): the stage that produces phi also writes the
+ * halo planes straight into the neighbouring slabs' ghost planes (peer
+ * stores over NVLink when the neighbour lives on another GPU).  Points
+ * within `ghost` of the slab's low z face are also written to lo_phi_out at
+ * z + lo_dz, points within `ghost` of the high face to hi_phi_out at
+ * z + hi_dz (normally lo_dz = +nz of the lower slab, hi_dz = -nz of this
+ * slab); x/y ghosts are refreshed periodically in every target.  Peer grids
+ * must share phi_out's row and plane strides.  Requires
+ * SB_LAUNCH_PERIODIC_GHOSTS. */
+typedef struct sb_zslab {
+    double *lo_phi_out;   /* origin of the lower neighbour's phi_out */
+    int32_t lo_dz;
+    double *hi_phi_out;   /* origin of the upper neighbour's phi_out */
+    int32_t hi_dz;
+} sb_zslab;
+
+SB_API int sb_rk4_stage_zslab(int32_t stage, const sb_rk4_fields *f, sb_space space, sb_rk4_constants c,
+                              sb_launch p, const sb_zslab *zs, void *stream);
+
 /* K6 — config-5 fused right-hand side: 24 inputs (ghost >= 2) -> 24 outputs. */
 SB_API int sb_rhs24(const sb_array *in, const sb_array *out, sb_space space,
              sb_d4_constants k, sb_poly poly, sb_launch p, void *stream);

@@ -28,7 +28,7 @@ EXPORTS = (
     "sb_abi_version", "sb_last_error", "sb_init", "sb_get_device_info", "sb_diff1d",
     "sb_lap7", "sb_d4_all", "sb_lap4_boxes", "sb_ghost_periodic", "sb_rk4_stage",
     "sb_rhs24", "sb_copy_regions", "sb_copy_h2d", "sb_copy_d2h", "sb_copy_h2d_planes", "sb_copy_d2h_planes",
-    "sb_copy_h2d_planes_staged",
+    "sb_copy_h2d_planes_staged", "sb_rk4_stage_zslab",
 )
 SB_MAX_COPY_JOBS = 64
 
@@ -63,6 +63,10 @@ class sb_rk4_constants(C.Structure):
     _fields_ = [("lap", sb_d4_constants), ("half_dt", C.c_double), ("dt", C.c_double), ("dt6", C.c_double)]
 
 
+class sb_zslab(C.Structure):
+    _fields_ = [("lo_phi_out", C.c_void_p), ("lo_dz", C.c_int32), ("hi_phi_out", C.c_void_p), ("hi_dz", C.c_int32)]
+
+
 class sb_poly(C.Structure):
     _fields_ = [("coef", C.c_void_p), ("p", C.c_void_p), ("q", C.c_void_p)]
 
@@ -94,6 +98,8 @@ def _declare(lib) -> None:
         "sb_lap4_boxes": ([C.POINTER(sb_box_job), i32, sb_d4_constants, sb_launch, vp], C.c_int),
         "sb_ghost_periodic": ([sb_array, vp], C.c_int),
         "sb_rk4_stage": ([i32, C.POINTER(sb_rk4_fields), sb_space, sb_rk4_constants, sb_launch, vp], C.c_int),
+        "sb_rk4_stage_zslab": ([i32, C.POINTER(sb_rk4_fields), sb_space, sb_rk4_constants, sb_launch,
+                                C.POINTER(sb_zslab), vp], C.c_int),
         "sb_rhs24": ([C.POINTER(sb_array), C.POINTER(sb_array), sb_space, sb_d4_constants, sb_poly, sb_launch, vp],
                      C.c_int),
         "sb_copy_regions": ([C.POINTER(sb_copy_job), i32, vp], C.c_int),

@@ -206,6 +206,11 @@ int sb_ghost_periodic(sb_array a, void *stream) {
 
 int sb_rk4_stage(int32_t stage, const sb_rk4_fields *f, sb_space space, sb_rk4_constants c, sb_launch p,
                  void *stream) {
+    return sb_rk4_stage_zslab(stage, f, space, c, p, nullptr, stream);
+}
+
+int sb_rk4_stage_zslab(int32_t stage, const sb_rk4_fields *f, sb_space space, sb_rk4_constants c, sb_launch p,
+                       const sb_zslab *zs, void *stream) {
     if (!f) return fail(SB_USAGE, "rk4_stage: null fields");
     if (stage < 1 || stage > 4) return fail(SB_USAGE, "rk4_stage: stage must be 1..4");
     int rc;
@@ -245,7 +250,9 @@ int sb_rk4_stage(int32_t stage, const sb_rk4_fields *f, sb_space space, sb_rk4_c
         mode = stage == 4 ? D4_RK4 : D4_RK23;
         ca = stage == 3 ? c.dt : c.dt6;
     }
-    return launch_d4(mode, &job, 1, c.lap, ca, 0.0, p, as_stream(stream));
+    if (zs && ((zs->lo_phi_out && !aligned16(zs->lo_phi_out)) || (zs->hi_phi_out && !aligned16(zs->hi_phi_out))))
+        return fail(SB_USAGE, "rk4_stage_zslab: peer origins must be 16-byte aligned");
+    return launch_d4(mode, &job, 1, c.lap, ca, 0.0, p, as_stream(stream), zs);
 }
 
 int sb_rhs24(const sb_array *in, const sb_array *out, sb_space space, sb_d4_constants k, sb_poly poly, sb_launch p,

@@ -61,6 +61,8 @@ struct D4Params {
     int pw_tma0[5][3];
     int per[3];                // periodic extents for fused ghost stores (0 = none)
     int pghost;                // ghost width refreshed by the fused stores
+    double *zlo, *zhi;         // z targets of points near the low / high face
+    int zlo_dz, zhi_dz;        //   and their z shifts (periodic box: same grid, +nz / -nz)
     int nbox;
     int ty, zc;
     double k1, k2, k11;
@@ -192,16 +194,31 @@ __device__ __forceinline__ int images(int c, int n, int g, int (&o)[3]) {
     return 1 + (int)lo + (int)hi;
 }
 
-// Rare path, kept out of line so the unrolled plane loop stays small.
+// Rare path, kept out of line so the unrolled plane loop stays small.  x/y
+// images stay in each target; z images go to the z targets (this grid when
+// the box is periodic in z, the neighbouring slabs' grids for a z-slab
+// decomposition).
 __device__ __noinline__ void store_images(double *base, long long sy, long long sz, int nx, int ny, int nz, int g,
-                                          int x, int y, int z, double v) {
-    int ox[3], oy[3], oz[3];
-    const int kx = images(x, nx, g, ox), ky = images(y, ny, g, oy), kz = images(z, nz, g, oz);
-    double *p0 = base + x + (long long)y * sy + (long long)z * sz;
-    for (int a = 0; a < kz; ++a)
+                                          double *zlo, int zlo_dz, double *zhi, int zhi_dz, int x, int y, int z,
+                                          double v) {
+    int ox[3], oy[3];
+    const int kx = images(x, nx, g, ox), ky = images(y, ny, g, oy);
+    double *tb[3];
+    int tz[3], kt = 0;
+    tb[kt] = base;
+    tz[kt++] = 0;
+    if (z < g && zlo) {
+        tb[kt] = zlo;
+        tz[kt++] = zlo_dz;
+    }
+    if (z >= nz - g && zhi) {
+        tb[kt] = zhi;
+        tz[kt++] = zhi_dz;
+    }
+    for (int t = 0; t < kt; ++t)
         for (int b = 0; b < ky; ++b)
             for (int d = 0; d < kx; ++d)
-                if (a | b | d) p0[ox[d] + (long long)oy[b] * sy + (long long)oz[a] * sz] = v;
+                if (t | b | d) tb[t][(x + ox[d]) + (long long)(y + oy[b]) * sy + (long long)(z + tz[t]) * sz] = v;
 }
 
 template <int NP>
@@ -211,7 +228,9 @@ __device__ __forceinline__ void store_periodic(double *base, long long sy, long 
     if (x >= g && x + NP <= P.per[0] - g && y >= g && y < P.per[1] - g && z >= g && z < P.per[2] - g) return;
 #pragma unroll
     for (int j = 0; j < NP; ++j)
-        if (L.m[j]) store_images(base, sy, sz, P.per[0], P.per[1], P.per[2], g, x + j, y, z, v[j]);
+        if (L.m[j])
+            store_images(base, sy, sz, P.per[0], P.per[1], P.per[2], g, P.zlo, P.zlo_dz, P.zhi, P.zhi_dz, x + j, y, z,
+                         v[j]);
 }
 
 template <int MODE, int TX, int NP, int R>
@@ -514,7 +533,7 @@ bool same_strides(const sb_array &a, const sb_array &b) { return a.sy == b.sy &&
 }  // namespace
 
 int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, double ca, double cb,
-              const sb_launch &p, cudaStream_t st) {
+              const sb_launch &p, cudaStream_t st, const sb_zslab *zslab) {
     (void)cb;
     if (njobs < 1 || njobs > SB_MAX_BOXES) return fail(SB_RESOURCE, "box count outside 1..SB_MAX_BOXES");
     const int TX = p.tile_x, TY = p.tile_y, ZC = p.z_chunk;
@@ -594,6 +613,18 @@ int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, 
         P.per[1] = O.ny;
         P.per[2] = O.nz;
         P.pghost = O.ghost;
+        if (zslab) {
+            P.zlo = zslab->lo_phi_out;
+            P.zlo_dz = zslab->lo_dz;
+            P.zhi = zslab->hi_phi_out;
+            P.zhi_dz = zslab->hi_dz;
+        } else {   // periodic in z within this grid
+            P.zlo = P.zhi = O.origin;
+            P.zlo_dz = O.nz;
+            P.zhi_dz = -O.nz;
+        }
+    } else if (zslab) {
+        return fail(SB_USAGE, "z-slab halo stores need SB_LAUNCH_PERIODIC_GHOSTS");
     }
     const int nb = (int)total;
     switch (mode) {

@@ -1,0 +1,152 @@
+"""F4 — z-slab decomposition of one periodic box.
+
+A 384^3 periodic box split along z into R slabs needs exactly one exchange
+per RK stage: the 2 planes next to each slab face go to the neighbouring
+slab's ghost planes.  Instead of a separate exchange step (pack, NCCL
+send/recv, unpack), the stage kernel that produces phi writes those planes
+straight into the neighbour's phi ghost planes as part of its stores
+(``sb_rk4_stage_zslab``): over NVLink when the neighbour is another GPU
+(peer-mapped pointers via CUDA IPC), as plain stores when it is another slab
+on the same GPU.  The only synchronisation left is "every slab finished
+stage s" before stage s+1 reads its ghosts — a barrier, no data movement.
+
+* :class:`WaveRK4Slabs` — R slabs in one process (one GPU): the fused
+  exchange exercised end to end without extra GPUs.
+* :class:`ZSlabRank` — one slab per process/rank; neighbour buffers are
+  mapped with CUDA IPC handles exchanged through ``torch.distributed``
+  objects, and ``barrier`` orders the stages across ranks.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+from . import _lib
+from .errors import UsageError
+from .grid import DeviceGrid, stream_ptr
+from .inputs import WaveConstants
+from .tuner import LaunchParams
+
+BUFFERS = ("phi0", "pi0", "phi_a", "pi_a", "phi_b", "pi_b", "acc_phi", "acc_pi")
+# (stage, phi_s, pi_s, phi_out, pi_out) of one classical RK4 step
+STAGES = ((1, "phi0", "pi0", "phi_a", "pi_a"), (2, "phi_a", "pi_a", "phi_b", "pi_b"),
+          (3, "phi_b", "pi_b", "phi_a", "pi_a"), (4, "phi_a", "pi_a", "phi_b", "pi_b"))
+
+
+def z_cuts(n: int, parts: int, ghost: int) -> list[int]:
+    """Even z cuts of [0, n) into `parts` slabs, each at least `ghost` thick."""
+    if parts < 1 or n // parts < ghost:
+        raise UsageError(f"{parts} slabs of a {n}-plane box would be thinner than the ghost width {ghost}")
+    return [n * j // parts for j in range(parts)] + [n]
+
+
+class Slab:
+    """One z-slab's RK4 state: interior (n, n, nz), ghost g, level z offset z0."""
+
+    def __init__(self, n: int, z0: int, nz: int, ghost: int, device=None):
+        self.n, self.z0, self.nz, self.g = n, z0, nz, ghost
+        for name in BUFFERS:
+            setattr(self, name, DeviceGrid((n, n, nz), ghost, device, lower=(0, 0, z0)))
+
+    def upload(self, phi_global, pi_global) -> None:
+        """Take this slab's planes (with z ghosts) from global ghosted arrays."""
+        g, z0, nz = self.g, self.z0, self.nz
+        self.phi0.upload(phi_global[z0:z0 + nz + 2 * g], with_ghosts=True)
+        self.pi0.upload(pi_global[z0:z0 + nz + 2 * g], with_ghosts=True)
+
+
+def _fields(s: Slab, phi_s: str, pi_s: str, phi_out: str, pi_out: str) -> _lib.sb_rk4_fields:
+    return _lib.sb_rk4_fields(getattr(s, phi_s).abi(), getattr(s, pi_s).abi(), s.phi0.abi(), s.pi0.abi(),
+                              s.acc_phi.abi(), s.acc_pi.abi(), getattr(s, phi_out).abi(), getattr(s, pi_out).abi())
+
+
+def _consts(c: WaveConstants) -> _lib.sb_rk4_constants:
+    return _lib.sb_rk4_constants(_lib.d4_constants(c.lap), c.half_dt, c.dt, c.dt6)
+
+
+def launch_stage(s: Slab, stage: tuple, c: WaveConstants, params: LaunchParams, lo_ptr: int, lo_dz: int,
+                 hi_ptr: int, hi_dz: int, stream=None) -> None:
+    st, phi_s, pi_s, phi_out, pi_out = stage
+    f = _fields(s, phi_s, pi_s, phi_out, pi_out)
+    zs = _lib.sb_zslab(lo_ptr, lo_dz, hi_ptr, hi_dz)
+    _lib.call("sb_rk4_stage_zslab", st, C.byref(f), _lib.space((0, 0, 0), (s.n, s.n, s.nz)), _consts(c),
+              _lib.launch_of(params, _lib.SB_LAUNCH_PERIODIC_GHOSTS), C.byref(zs), stream_ptr(stream))
+
+
+class WaveRK4Slabs:
+    """R z-slabs of one periodic n^3 box in one process.  Each stage launch of
+    slab r writes its boundary planes into slabs r-1 / r+1 (ring)."""
+
+    def __init__(self, n: int, parts: int, ghost: int, c: WaveConstants, device=None):
+        self.n, self.g, self.c = n, ghost, c
+        cuts = z_cuts(n, parts, ghost)
+        self.slabs = [Slab(n, cuts[j], cuts[j + 1] - cuts[j], ghost, device) for j in range(parts)]
+        self.params = LaunchParams(64, 4, 16, 1)
+
+    def upload(self, phi_global, pi_global) -> None:
+        for s in self.slabs:
+            s.upload(phi_global, pi_global)
+
+    def step(self, params: LaunchParams | None = None, stream=None) -> None:
+        p = params or self.params
+        R = len(self.slabs)
+        for stage in STAGES:
+            out = stage[3]
+            for r, s in enumerate(self.slabs):
+                lo, hi = self.slabs[(r - 1) % R], self.slabs[(r + 1) % R]
+                launch_stage(s, stage, self.c, p, getattr(lo, out).origin_ptr, lo.nz,
+                             getattr(hi, out).origin_ptr, -s.nz, stream)
+
+    def result(self, name: str = "phi_b", with_ghosts: bool = False):
+        import numpy as np
+        parts = [getattr(s, name).download(with_ghosts=with_ghosts) for s in self.slabs]
+        if not with_ghosts:
+            return np.concatenate(parts, axis=0)
+        return parts
+
+
+class ZSlabRank:
+    """This rank's slab of a z-decomposed periodic box (one slab per rank).
+
+    Neighbour buffers are CUDA-IPC-mapped (peer memory over NVLink on a
+    multi-GPU node); ``dist`` is an initialised ``torch.distributed``
+    module/group for the handle exchange and ``barrier()`` orders stages."""
+
+    def __init__(self, n: int, rank: int, world: int, ghost: int, c: WaveConstants, dist, device=None):
+        import torch
+        self.n, self.g, self.c = n, ghost, c
+        self.rank, self.world, self.dist = rank, world, dist
+        cuts = z_cuts(n, world, ghost)
+        self.slab = Slab(n, cuts[rank], cuts[rank + 1] - cuts[rank], ghost, device)
+        self.params = LaunchParams(64, 4, 16, 1)
+        mine = {name: (getattr(self.slab, name).storage.untyped_storage()._share_cuda_(),
+                       getattr(self.slab, name).offset) for name in ("phi_a", "phi_b")}
+        everyone = [None] * world
+        dist.all_gather_object(everyone, (self.slab.nz, mine))
+        self._keep = []
+        self.peer: dict[tuple[int, str], int] = {}
+        self.peer_nz: dict[int, int] = {}
+        for r in {(rank - 1) % world, (rank + 1) % world}:
+            nz_r, handles = everyone[r]
+            self.peer_nz[r] = nz_r
+            for name, (h, off) in handles.items():
+                if r == rank:
+                    ptr = getattr(self.slab, name).origin_ptr
+                else:
+                    st = torch.UntypedStorage._new_shared_cuda(*h)
+                    self._keep.append(st)
+                    ptr = st.data_ptr() + 8 * off
+                self.peer[(r, name)] = ptr
+
+    def barrier(self) -> None:
+        import torch
+        torch.cuda.synchronize()
+        self.dist.barrier()
+
+    def step(self, params: LaunchParams | None = None) -> None:
+        p = params or self.params
+        lo, hi = (self.rank - 1) % self.world, (self.rank + 1) % self.world
+        for stage in STAGES:
+            out = stage[3]
+            launch_stage(self.slab, stage, self.c, p, self.peer[(lo, out)], self.peer_nz[lo],
+                         self.peer[(hi, out)], -self.slab.nz)
+            self.barrier()
