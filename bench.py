@@ -189,11 +189,16 @@ def run_ours(args) -> None:
     import torch
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
+    dev = local % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
     dist = None
+    backend = os.environ.get("STENCIL_BENCH_BACKEND", "nccl")   # gloo: plumbing test with ranks sharing a GPU
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
 
     from paper_1308_1343_b200 import _build
     from paper_1308_1343_b200.configs import C2FourthOrder
@@ -252,7 +257,7 @@ def run_ours(args) -> None:
     def max_over_ranks(x: float) -> float:
         if not dist:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -260,7 +265,7 @@ def run_ours(args) -> None:
         prob.run(params)
     barrier()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         ev[0].record(stream)
         for i in range(args.steps):
             prob.run(params)
@@ -284,7 +289,7 @@ def run_ours(args) -> None:
         prob.e2e_step(h_in.data_ptr(), out_ptrs, params)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk_e2e:
+    with ClockSampler(dev) as clk_e2e:
         e0.record(stream)
         for _ in range(e2e_steps):
             prob.e2e_step(h_in.data_ptr(), out_ptrs, params)
