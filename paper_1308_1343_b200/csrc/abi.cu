@@ -175,7 +175,7 @@ int sb_d4_all(const sb_array *out, sb_array src, sb_space space, sb_d4_constants
             return rc;
         job.g[i] = out[i];
     }
-    return launch_d4(D4_ALL10, &job, 1, k, 0.0, 0.0, p, as_stream(stream));
+    return launch_d4(D4_ALL10, &job, 1, k, 0.0, p, as_stream(stream));
 }
 
 int sb_lap4_boxes(const sb_box_job *jobs, int32_t njobs, sb_d4_constants k, sb_launch p, void *stream) {
@@ -195,7 +195,7 @@ int sb_lap4_boxes(const sb_box_job *jobs, int32_t njobs, sb_d4_constants k, sb_l
         dj[j].space = jobs[j].space;
         dj[j].g[0] = jobs[j].dst;
     }
-    return launch_d4(D4_LAP4, dj, njobs, k, 0.0, 0.0, p, as_stream(stream));
+    return launch_d4(D4_LAP4, dj, njobs, k, 0.0, p, as_stream(stream));
 }
 
 int sb_ghost_periodic(sb_array a, void *stream) {
@@ -252,7 +252,7 @@ int sb_rk4_stage_zslab(int32_t stage, const sb_rk4_fields *f, sb_space space, sb
     }
     if (zs && ((zs->lo_phi_out && !aligned16(zs->lo_phi_out)) || (zs->hi_phi_out && !aligned16(zs->hi_phi_out))))
         return fail(SB_USAGE, "rk4_stage_zslab: peer origins must be 16-byte aligned");
-    return launch_d4(mode, &job, 1, c.lap, ca, 0.0, p, as_stream(stream), zs);
+    return launch_d4(mode, &job, 1, c.lap, ca, p, as_stream(stream), zs);
 }
 
 int sb_rhs24(const sb_array *in, const sb_array *out, sb_space space, sb_d4_constants k, sb_poly poly, sb_launch p,

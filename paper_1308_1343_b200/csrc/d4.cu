@@ -108,22 +108,6 @@ __device__ __forceinline__ void store(double *p, const double (&v)[NP], const La
     }
 }
 
-template <int NP>
-__device__ __forceinline__ void load(const double *p, double (&v)[NP], const Lanes<NP> &L) {
-    if constexpr (NP == 2) {
-        if (L.full) {
-            const double2 t = load_pair(p);
-            v[0] = t.x;
-            v[1] = t.y;
-        } else {
-            v[0] = L.m[0] ? p[0] : 0.0;
-            v[1] = L.m[1] ? p[1] : 0.0;
-        }
-    } else {
-        v[0] = L.m[0] ? p[0] : 0.0;
-    }
-}
-
 // Row values x-2 .. x+NP+1 of shared-memory row `r` starting at column c (= x-2).
 template <int NP>
 __device__ __forceinline__ void row_vals(const double *r, double (&v)[NP + 4]) {
@@ -532,9 +516,8 @@ bool same_strides(const sb_array &a, const sb_array &b) { return a.sy == b.sy &&
 
 }  // namespace
 
-int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, double ca, double cb,
-              const sb_launch &p, cudaStream_t st, const sb_zslab *zslab) {
-    (void)cb;
+int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, double ca, const sb_launch &p,
+              cudaStream_t st, const sb_zslab *zslab) {
     if (njobs < 1 || njobs > SB_MAX_BOXES) return fail(SB_RESOURCE, "box count outside 1..SB_MAX_BOXES");
     const int TX = p.tile_x, TY = p.tile_y, ZC = p.z_chunk;
     const int NP = (p.flags & SB_LAUNCH_SCALAR) ? 1 : 2;

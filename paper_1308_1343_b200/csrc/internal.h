@@ -34,8 +34,8 @@ struct D4Job {
     sb_array g[10];       // mode-dependent outputs / pointwise inputs
 };
 
-int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, double ca, double cb,
-              const sb_launch &p, cudaStream_t st, const sb_zslab *zslab = nullptr);
+int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, double ca, const sb_launch &p,
+              cudaStream_t st, const sb_zslab *zslab = nullptr);
 
 int launch_ghost_periodic(const sb_array &a, cudaStream_t st);
 
