@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--shapes", default="all")
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--graph", action="store_true", help="time reps launches captured in one CUDA graph")
+    ap.add_argument("--flags", type=int, default=0, help="extra SB_LAUNCH_* flags for the kernel")
     args = ap.parse_args()
 
     import torch
@@ -36,6 +37,8 @@ def main():
     kw = {"n": args.n} if args.n else {}
     prob = CONFIGS[args.config](**kw).setup()
     kern = getattr(prob, "kernel", None)
+    if kern is not None and args.flags:
+        kern.extra_flags = args.flags
     if kern is not None:
         space = kern.launch_space()
         ext = kern.full_space().extents
