@@ -42,6 +42,12 @@ __host__ __device__ constexpr int max_threads(int mode, int np) {
     return (np == 2 && mode != D4_LAP4) ? 256 : 512;
 }
 
+// Minimum resident CTAs (of max_threads) the register allocation must allow.
+#ifndef SB_D4_ALL10_MINB
+#define SB_D4_ALL10_MINB 1
+#endif
+__host__ __device__ constexpr int min_blocks(int mode) { return mode == D4_ALL10 ? SB_D4_ALL10_MINB : 1; }
+
 struct BoxDesc {
     CUtensorMap tmap;          // plane boxes of (TX+4) x (TY+4) x 1 over the source grid
     double *g[10];             // mode-dependent outputs / pointwise inputs (origins)
@@ -399,7 +405,7 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
 }
 
 template <int MODE, int TX, int NP>
-__global__ void __launch_bounds__(max_threads(MODE, NP), 1) d4_kernel(const __grid_constant__ D4Params P) {
+__global__ void __launch_bounds__(max_threads(MODE, NP), min_blocks(MODE)) d4_kernel(const __grid_constant__ D4Params P) {
     constexpr int TPR = TX / NP;    // threads per row
     constexpr int W = TX + 4;       // smem row width (elements)
     extern __shared__ __align__(1024) unsigned char smem[];

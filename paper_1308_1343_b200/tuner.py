@@ -92,6 +92,16 @@ class TopologyConfig:
     def cache_line_elems(self) -> int:
         return max(1, self.cache_line_bytes // 8)
 
+    def with_device(self) -> "TopologyConfig":
+        """This topology with sm_count / shared memory / L2 of the current
+        CUDA device (the run-time discovery the reference leaves to a file,
+        tuner.py:38-40)."""
+        from . import _lib
+        info = _lib.sb_device_info()
+        _lib.call("sb_get_device_info", _lib.C.byref(info))
+        return replace(self, sm_count=int(info.sm_count), smem_per_block=int(info.smem_optin_bytes),
+                       l2_bytes=int(info.l2_bytes))
+
 
 @dataclass(frozen=True)
 class LoopSetup:

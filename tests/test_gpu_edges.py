@@ -115,3 +115,9 @@ def test_level_with_many_boxes_chunks_launches():
         want = np.empty((nz, ny, nx))
         oracle.lap4(want, u, 2, (0, nx, 0, ny, 0, nz), p.k.k2)
         assert same(got, want), b
+
+
+def test_topology_from_device():
+    from paper_1308_1343_b200.tuner import TopologyConfig
+    t = TopologyConfig().with_device()
+    assert t.sm_count >= 100 and t.smem_per_block >= 200 * 1024 and t.l2_bytes > 50 * 2 ** 20
