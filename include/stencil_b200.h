@@ -184,6 +184,17 @@ SB_API int sb_ghost_periodic(sb_array a, void *stream);
 SB_API int sb_rk4_stage(int32_t stage, const sb_rk4_fields *f, sb_space space,
                  sb_rk4_constants c, sb_launch p, void *stream);
 
+/* K5b — the same RK4 step as two fused launches (temporal blocking):
+ * pair 1 = stages 1+2: reads phi0, pi0 (ghosts valid), writes phi_out = phi3,
+ *   pi_out = pi3, acc_phi = pi0 + 2 pi2, acc_pi = L1 + 2 L2;
+ * pair 2 = stages 3+4: reads phi_s = phi3, phi0, pi_s = pi3 (ghosts valid),
+ *   pi0, acc_phi, acc_pi, writes phi_out = phi', pi_out = pi'.
+ * Bit-identical to the four sb_rk4_stage launches; 14 array passes instead
+ * of 32.  With SB_LAUNCH_PERIODIC_GHOSTS both phi_out and pi_out get their
+ * periodic ghost shells refreshed (pi's ghosts feed the next pair). */
+SB_API int sb_rk4_pair(int32_t pair, const sb_rk4_fields *f, sb_space space, sb_rk4_constants c, sb_launch p,
+                       void *stream);
+
 /* F4 — z-slab decomposition of one periodic box over several GPUs (or
  * several slabs of one GPU): the stage that produces phi also writes the
  * halo planes straight into the neighbouring slabs' ghost planes (peer

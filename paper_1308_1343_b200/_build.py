@@ -19,8 +19,8 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 INCLUDE = PKG.parent / "include"
 LIB = PKG / "libstencil_b200.so"
-SOURCES = ["abi.cu", "lap7.cu", "d4.cu", "ghost.cu", "rhs24.cu", "regions.cu"]
-HEADERS = ["common.cuh", "internal.h"]
+SOURCES = ["abi.cu", "lap7.cu", "d4.cu", "rkpair.cu", "ghost.cu", "rhs24.cu", "regions.cu"]
+HEADERS = ["common.cuh", "internal.h", "stencil_ops.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [

@@ -108,28 +108,34 @@ class C3WaveRK4:
 
     name = "c3_wave_rk4"
 
-    def __init__(self, n: int = 384, seed: int | None = None, g: int = 2, fused_ghosts: bool = True):
+    def __init__(self, n: int = 384, seed: int | None = None, g: int = 2, schedule: str = "pairs"):
         self.n, self.g = n, g
-        self.fused_ghosts = fused_ghosts
+        self.schedule = schedule
         self.host_phi, self.host_pi = inputs.c3_fields(n, g, seed)
         self.c = inputs.WaveConstants.for_grid(n)
         self.updates = n ** 3
-        # array passes over the interior + the ghost shell of the 4 ghosted phi_s reads.
-        # SURVEY.md §8(d) counts 34 passes; this algorithm needs 32: stage 1 no
-        # longer materialises acc_phi = pi0 (stage 2 forms pi0 + 2 pi_s from the
-        # pi0 it reads anyway), i.e. stage reads+writes 2+3, 5+4, 6+4, 6+2.
-        self.canonical_bytes = 8 * (32 * n ** 3 + 4 * (_vol((n,) * 3, g) - n ** 3))
-        self.survey_canonical_bytes = 8 * (34 * n ** 3 + 4 * (_vol((n,) * 3, g) - n ** 3))
+        # array passes over the interior + the ghost shells of the ghosted reads.
+        # SURVEY.md §8(d) counts 34 passes (four stage sweeps); the four-stage
+        # schedule here needs 32 (stage 1 does not materialise acc_phi = pi0),
+        # the fused pair schedule 14: pair 1 reads phi0, pi0 (ghosted) and
+        # writes phi3, pi3, acc_phi, acc_pi; pair 2 reads phi3, phi0, pi3
+        # (ghosted), pi0, acc_phi, acc_pi and writes phi', pi'.
+        shell = _vol((n,) * 3, g) - n ** 3
+        passes, ghosted = {"pairs": (14, 5), "stages": (32, 4), "stages_unfused": (32, 4)}[schedule]
+        self.canonical_bytes = 8 * (passes * n ** 3 + ghosted * shell)
+        self.survey_canonical_bytes = 8 * (34 * n ** 3 + 4 * shell)
         self.ghost_fill_bytes = 8 * 4 * 2 * (_vol((n,) * 3, g) - n ** 3)
 
     def setup(self, device=None):
-        self.rk = WaveRK4(self.n, self.g, self.c, device, fused_ghosts=self.fused_ghosts)
+        self.rk = WaveRK4(self.n, self.g, self.c, device, schedule=self.schedule)
         self.reset()
         return self
 
     def reset(self):
         self.rk.phi0.upload(self.host_phi, with_ghosts=True)
         self.rk.pi0.upload(self.host_pi, with_ghosts=True)
+        self.rk.fill_ghosts(self.rk.phi0)
+        self.rk.fill_ghosts(self.rk.pi0)
 
     def run(self, params: LaunchParams | None = None, stream=None) -> None:
         self.rk.step(params, stream)

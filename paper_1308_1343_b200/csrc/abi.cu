@@ -255,6 +255,48 @@ int sb_rk4_stage_zslab(int32_t stage, const sb_rk4_fields *f, sb_space space, sb
     return launch_d4(mode, &job, 1, c.lap, ca, p, as_stream(stream), zs);
 }
 
+int sb_rk4_pair(int32_t pair, const sb_rk4_fields *f, sb_space space, sb_rk4_constants c, sb_launch p,
+                void *stream) {
+    if (!f) return fail(SB_USAGE, "rk4_pair: null fields");
+    if (pair != 1 && pair != 2) return fail(SB_USAGE, "rk4_pair: pair must be 1 (stages 1+2) or 2 (stages 3+4)");
+    sb_array halo[3], tile[3], out[4];
+    int nh, nt, no;
+    if (pair == 1) {
+        halo[0] = f->phi0;
+        halo[1] = f->pi0;
+        nh = 2;
+        nt = 0;
+        out[0] = f->phi_out;
+        out[1] = f->pi_out;
+        out[2] = f->acc_phi;
+        out[3] = f->acc_pi;
+        no = 4;
+    } else {
+        halo[0] = f->phi_s;
+        halo[1] = f->phi0;
+        halo[2] = f->pi_s;
+        nh = 3;
+        tile[0] = f->pi0;
+        tile[1] = f->acc_phi;
+        tile[2] = f->acc_pi;
+        nt = 3;
+        out[0] = f->phi_out;
+        out[1] = f->pi_out;
+        no = 2;
+    }
+    int rc;
+    for (int h = 0; h < nh; ++h)
+        if ((rc = check_array(halo[h], 2, "rk4_pair halo input")) || (rc = check_space(space, halo[h], "rk4_pair")))
+            return rc;
+    for (int t = 0; t < nt; ++t)
+        if ((rc = check_array(tile[t], 0, "rk4_pair input")) || (rc = check_space(space, tile[t], "rk4_pair")))
+            return rc;
+    for (int o = 0; o < no; ++o)
+        if ((rc = check_array(out[o], 0, "rk4_pair output")) || (rc = check_space(space, out[o], "rk4_pair")))
+            return rc;
+    return launch_rk4_pair(pair - 1, halo, nh, tile, nt, out, no, space, c, p, as_stream(stream));
+}
+
 int sb_rhs24(const sb_array *in, const sb_array *out, sb_space space, sb_d4_constants k, sb_poly poly, sb_launch p,
              void *stream) {
     if (!in || !out) return fail(SB_USAGE, "rhs24: null array table");

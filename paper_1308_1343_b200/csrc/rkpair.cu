@@ -1,0 +1,408 @@
+// rkpair.cu — K5b: classical RK4 for d/dt(phi, pi) = (pi, Lap4 phi) with the
+// stages fused in pairs (temporal blocking), two launches per step.
+//
+// The RK right-hand side only differentiates phi, and each stage's phi is a
+// pointwise combination of phi0 and the previous pi:
+//     phi2 = phi0 + (dt/2) pi0,   phi4 = phi0 + dt pi3.
+// So stage 2's Laplacian of phi2 needs only phi0 and pi0 within the stencil
+// radius, and stage 4's Laplacian of phi4 only phi0 and pi3 — the ghost width
+// of 2 suffices and no intermediate phi ever has to reach HBM:
+//   pair A (stages 1+2): reads phi0, pi0 (with halo);
+//                        writes phi3, pi3, acc_phi = pi0 + 2 pi2, acc_pi = L1 + 2 L2;
+//   pair B (stages 3+4): reads phi3, phi0, pi3 (with halo), pi0, acc_phi, acc_pi;
+//                        writes phi', pi'.
+// 14 array passes per step instead of 32 for four separate stage sweeps.
+// Every value is produced by exactly the expression tree the per-stage
+// kernels (d4.cu, mode RK1/RK2/RK23/RK4) and the oracle (oracle/stencils.py:
+// rk4_step) use — the derived phi2 / phi4 are formed in registers from the
+// staged planes with the same single rounding per operation — so the results
+// are bit-identical to the four-stage path.
+//
+// Structure as in d4.cu: a CTA owns a TX x TY column tile and streams z; every
+// plane of the halo inputs ((TX+4) x (TY+4)) and, once outputs start, the
+// tile planes of the pointwise inputs arrive by TMA in a 4-stage ring; z
+// terms come from five-slot register rings (loop unrolled five ways); the
+// producing stores also refresh the periodic ghost images of phi and pi.
+#include <cstring>
+
+#include "common.cuh"
+#include "internal.h"
+#include "stencil_ops.cuh"
+
+namespace sb {
+
+namespace {
+
+using namespace ops;
+
+constexpr int kStages = 4;
+enum { PAIR_A = 0, PAIR_B = 1 };
+
+__host__ __device__ constexpr int n_halo(int pair) { return pair == PAIR_A ? 2 : 3; }
+__host__ __device__ constexpr int n_tile(int pair) { return pair == PAIR_A ? 0 : 3; }
+__host__ __device__ constexpr int max_threads_pair(int np) { return np == 2 ? 256 : 512; }
+
+struct PairParams {
+    CUtensorMap hmap[3];       // (TX+4) x (TY+4) x 1 boxes: A: phi0, pi0   B: phi3, phi0, pi3
+    CUtensorMap tmap[3];       // TX x TY x 1 boxes:         B: pi0, acc_phi, acc_pi
+    int htma0[3][3], ttma0[3][3];
+    double *out[4];            // A: phi3, pi3, acc_phi, acc_pi   B: phi', pi'
+    long long sy, sz;          // strides shared by the outputs
+    int lo[3], hi[3];
+    int ax0, ntx, nty, ty, zc;
+    double k2, hdt, dt, dt6;
+    int per[3], pghost;        // periodic extents (0: no ghost refresh) and ghost width
+};
+
+struct PCtx {
+    const double *stages;
+    uint64_t *full;
+    int plane_elems, tile_elems, stage_elems, H, TY, nthr, tid, cx, ry;
+    int X0, Y0, Z0, Z1, nplanes;
+    long long off_xy;
+};
+
+template <int NP>
+struct PRings {
+    double ua[5][NP], sa[5][NP];   // A: phi0       B: phi3   (value, Dxx + Dyy)
+    double ub[5][NP], sb[5][NP];   // A: phi2       B: phi4
+    double c1[5][NP];              // A: pi0        B: phi0   (centre values)
+    double c2[5][NP];              //               B: pi3
+};
+
+template <int PAIR, int TX>
+__device__ __forceinline__ void issue(const PCtx &c, const PairParams &P, int j, int s) {
+    constexpr int NH = n_halo(PAIR), NT = n_tile(PAIR);
+    double *st = const_cast<double *>(c.stages) + s * c.stage_elems;
+    const bool with_tile = NT > 0 && j >= 4;
+    const uint32_t bytes = (uint32_t)(NH * (TX + 4) * c.H * 8 + (with_tile ? NT * TX * c.TY * 8 : 0));
+    mbar_arrive_expect_tx(&c.full[s], bytes);
+#pragma unroll
+    for (int h = 0; h < NH; ++h)
+        tma_load_3d(st + h * c.plane_elems, &P.hmap[h], P.htma0[h][0] + c.X0 - 2, P.htma0[h][1] + c.Y0 - 2,
+                    P.htma0[h][2] + c.Z0 - 2 + j, &c.full[s]);
+    if constexpr (NT > 0) {
+        if (with_tile) {
+            const int zc = c.Z0 - 4 + j;
+#pragma unroll
+            for (int t = 0; t < NT; ++t)
+                tma_load_3d(st + NH * c.plane_elems + t * c.tile_elems, &P.tmap[t], P.ttma0[t][0] + c.X0,
+                            P.ttma0[t][1] + c.Y0, P.ttma0[t][2] + zc, &c.full[s]);
+        }
+    }
+}
+
+// The thread's stencil neighbourhood in one staged plane: row x-2..x+NP+1
+// and the y neighbours y-2, y-1, y+1, y+2 of its NP points.
+template <int TX, int NP>
+struct Nbhd {
+    double xr[NP + 4], ym2[NP], ym1[NP], yp1[NP], yp2[NP];
+    __device__ __forceinline__ void load(const double *pl, int ry, int cx) {
+        constexpr int W = TX + 4;
+        row_vals<NP>(pl + (ry + 2) * W + NP * cx, xr);
+        col_vals<NP>(pl + (ry + 0) * W + NP * cx + 2, ym2);
+        col_vals<NP>(pl + (ry + 1) * W + NP * cx + 2, ym1);
+        col_vals<NP>(pl + (ry + 3) * W + NP * cx + 2, yp1);
+        col_vals<NP>(pl + (ry + 4) * W + NP * cx + 2, yp2);
+    }
+    // this = a + c * b, elementwise (the derived stage field phi0 + c pi)
+    __device__ __forceinline__ void combine(const Nbhd &a, double cc, const Nbhd &b) {
+#pragma unroll
+        for (int k = 0; k < NP + 4; ++k) xr[k] = add(a.xr[k], mul(cc, b.xr[k]));
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            ym2[j] = add(a.ym2[j], mul(cc, b.ym2[j]));
+            ym1[j] = add(a.ym1[j], mul(cc, b.ym1[j]));
+            yp1[j] = add(a.yp1[j], mul(cc, b.yp1[j]));
+            yp2[j] = add(a.yp2[j], mul(cc, b.yp2[j]));
+        }
+    }
+    // Dxx + Dyy at the thread's points
+    __device__ __forceinline__ void lap_xy(double k2, double (&s)[NP]) const {
+#pragma unroll
+        for (int j = 0; j < NP; ++j)
+            s[j] = add(d2(xr[j], xr[j + 1], xr[j + 2], xr[j + 3], xr[j + 4], k2),
+                       d2(ym2[j], ym1[j], xr[j + 2], yp1[j], yp2[j], k2));
+    }
+};
+
+template <int NP>
+__device__ __forceinline__ void out_periodic(const PairParams &P, double *base, long long off, int x, int y, int z,
+                                             const double (&v)[NP], const Lanes<NP> &L) {
+    store<NP>(base + off, v, L);
+    if (!P.per[0]) return;
+    const int g = P.pghost;
+    if (x >= g && x + NP <= P.per[0] - g && y >= g && y < P.per[1] - g && z >= g && z < P.per[2] - g) return;
+#pragma unroll
+    for (int j = 0; j < NP; ++j)
+        if (L.m[j])
+            store_images(base, P.sy, P.sz, P.per[0], P.per[1], P.per[2], g, base, P.per[2], base, -P.per[2], x + j,
+                         y, z, v[j]);
+}
+
+template <int PAIR, int TX, int NP, int R>
+__device__ __forceinline__ bool pair_plane(int i, const PCtx &c, const PairParams &P, const Lanes<NP> &L,
+                                           PRings<NP> &rg) {
+    constexpr int NH = n_halo(PAIR);
+    if (i >= c.nplanes) return true;
+    const int s = i & (kStages - 1);
+    const int z = c.Z0 - 2 + i;
+    const int zc = z - 2;
+    mbar_wait(&c.full[s], (i / kStages) & 1);
+    const double *pl = c.stages + s * c.stage_elems;
+
+    double tv[3][NP];   // B: pi0, acc_phi, acc_pi at the thread's points of plane zc
+    {
+        Nbhd<TX, NP> a, b, d;
+        a.load(pl, c.ry, c.cx);                       // A: phi0   B: phi3
+        b.load(pl + c.plane_elems, c.ry, c.cx);       // A: pi0    B: phi0
+        double sa[NP], sb2[NP];
+        a.lap_xy(P.k2, sa);
+        if constexpr (PAIR == PAIR_A) {
+            d.combine(a, P.hdt, b);                   // phi2 = phi0 + (dt/2) pi0
+            d.lap_xy(P.k2, sb2);
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                rg.ua[R][j] = a.xr[j + 2];
+                rg.sa[R][j] = sa[j];
+                rg.ub[R][j] = d.xr[j + 2];
+                rg.sb[R][j] = sb2[j];
+                rg.c1[R][j] = b.xr[j + 2];
+            }
+        } else {
+            Nbhd<TX, NP> p3;
+            p3.load(pl + 2 * c.plane_elems, c.ry, c.cx);   // pi3
+            d.combine(b, P.dt, p3);                   // phi4 = phi0 + dt pi3
+            d.lap_xy(P.k2, sb2);
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                rg.ua[R][j] = a.xr[j + 2];
+                rg.sa[R][j] = sa[j];
+                rg.ub[R][j] = d.xr[j + 2];
+                rg.sb[R][j] = sb2[j];
+                rg.c1[R][j] = b.xr[j + 2];
+                rg.c2[R][j] = p3.xr[j + 2];
+            }
+            if (i >= 4) {
+#pragma unroll
+                for (int t = 0; t < 3; ++t)
+                    col_vals<NP>(pl + NH * c.plane_elems + t * c.tile_elems + c.ry * TX + NP * c.cx, tv[t]);
+            }
+        }
+    }
+
+    named_bar(1, c.nthr);   // every thread is done with stage s
+    if (c.tid == 0 && i + kStages < c.nplanes) issue<PAIR, TX>(c, P, i + kStages, s);
+    if (i < 4) return false;
+
+    constexpr int K0 = (R + 1) % 5, K1 = (R + 2) % 5, K2 = (R + 3) % 5, K3 = (R + 4) % 5, K4 = R;
+    const long long offc = c.off_xy + (long long)zc * P.sz;
+    const int x = c.X0 + NP * c.cx, y = c.Y0 + c.ry;
+    double la[NP], lb[NP];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+        la[j] = add(rg.sa[K2][j], d2(rg.ua[K0][j], rg.ua[K1][j], rg.ua[K2][j], rg.ua[K3][j], rg.ua[K4][j], P.k2));
+        lb[j] = add(rg.sb[K2][j], d2(rg.ub[K0][j], rg.ub[K1][j], rg.ub[K2][j], rg.ub[K3][j], rg.ub[K4][j], P.k2));
+    }
+    if constexpr (PAIR == PAIR_A) {
+        // stage 1: pi2 = pi0 + (dt/2) L1          stage 2: phi3 = phi0 + (dt/2) pi2
+        //          (acc_pi = L1)                           pi3  = pi0 + (dt/2) L2
+        //                                                  acc_phi = pi0 + 2 pi2, acc_pi = L1 + 2 L2
+        double f3[NP], p3[NP], af[NP], ap[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            const double phi0 = rg.ua[K2][j], pi0 = rg.c1[K2][j];
+            const double pi2 = add(pi0, mul(P.hdt, la[j]));
+            f3[j] = add(phi0, mul(P.hdt, pi2));
+            p3[j] = add(pi0, mul(P.hdt, lb[j]));
+            af[j] = add(pi0, mul(2.0, pi2));
+            ap[j] = add(la[j], mul(2.0, lb[j]));
+        }
+        out_periodic<NP>(P, P.out[0], offc, x, y, zc, f3, L);
+        out_periodic<NP>(P, P.out[1], offc, x, y, zc, p3, L);
+        store<NP>(P.out[2] + offc, af, L);
+        store<NP>(P.out[3] + offc, ap, L);
+    } else {
+        // stage 3: pi4 = pi0 + dt L3, acc_phi += 2 pi3, acc_pi += 2 L3   (phi4 = phi0 + dt pi3)
+        // stage 4: phi' = phi0 + (dt/6)(acc_phi + pi4), pi' = pi0 + (dt/6)(acc_pi + L4)
+        double fn[NP], pn[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            const double phi0 = rg.c1[K2][j], pi3 = rg.c2[K2][j];
+            const double pi0 = tv[0][j], acf = tv[1][j], acp = tv[2][j];
+            const double pi4 = add(pi0, mul(P.dt, la[j]));
+            const double acf3 = add(acf, mul(2.0, pi3));
+            const double acp3 = add(acp, mul(2.0, la[j]));
+            fn[j] = add(phi0, mul(P.dt6, add(acf3, pi4)));
+            pn[j] = add(pi0, mul(P.dt6, add(acp3, lb[j])));
+        }
+        out_periodic<NP>(P, P.out[0], offc, x, y, zc, fn, L);
+        out_periodic<NP>(P, P.out[1], offc, x, y, zc, pn, L);
+    }
+    return false;
+}
+
+template <int PAIR, int TX, int NP>
+__global__ void __launch_bounds__(max_threads_pair(NP), 1) rkpair_kernel(const __grid_constant__ PairParams P) {
+    constexpr int TPR = TX / NP;
+    constexpr int W = TX + 4;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    PCtx c;
+    c.TY = P.ty;
+    c.H = c.TY + 4;
+    c.nthr = TPR * c.TY;
+    c.plane_elems = round_up(W * c.H, 16);
+    c.tile_elems = round_up(TX * c.TY, 16);
+    c.stage_elems = n_halo(PAIR) * c.plane_elems + n_tile(PAIR) * c.tile_elems;
+    c.full = reinterpret_cast<uint64_t *>(smem);
+    c.stages = reinterpret_cast<const double *>(smem + 128);
+
+    int t = blockIdx.x;
+    const int bx = t % P.ntx;
+    t /= P.ntx;
+    const int by = t % P.nty;
+    const int bz = t / P.nty;
+    c.X0 = P.ax0 + bx * TX;
+    c.Y0 = P.lo[1] + by * c.TY;
+    c.Z0 = P.lo[2] + bz * P.zc;
+    c.Z1 = min(c.Z0 + P.zc, P.hi[2]);
+    c.nplanes = c.Z1 - c.Z0 + 4;
+    c.tid = threadIdx.x;
+    c.cx = c.tid % TPR;
+    c.ry = c.tid / TPR;
+    const int x = c.X0 + NP * c.cx, y = c.Y0 + c.ry;
+    c.off_xy = (long long)x + (long long)y * P.sy;
+    Lanes<NP> L;
+    const bool yin = y < P.hi[1];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) L.m[j] = (yin && x + j >= P.lo[0] && x + j < P.hi[0]) ? 1 : 0;
+    if constexpr (NP == 2) {
+        L.full = L.m[0] & L.m[1];
+        L.only0 = L.m[0] & (L.m[1] ^ 1);
+        L.only1 = L.m[1] & (L.m[0] ^ 1);
+    }
+
+    if (c.tid == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&c.full[s], 1);
+        fence_mbar_init();
+        for (int i = 0; i < kStages && i < c.nplanes; ++i) issue<PAIR, TX>(c, P, i, i);
+    }
+    __syncthreads();
+
+    PRings<NP> rg;
+#pragma unroll
+    for (int k = 0; k < 5; ++k)
+#pragma unroll
+        for (int j = 0; j < NP; ++j)
+            rg.ua[k][j] = rg.sa[k][j] = rg.ub[k][j] = rg.sb[k][j] = rg.c1[k][j] = rg.c2[k][j] = 0.0;
+    for (int i = 0;; i += 5) {
+        if (pair_plane<PAIR, TX, NP, 0>(i + 0, c, P, L, rg)) break;
+        if (pair_plane<PAIR, TX, NP, 1>(i + 1, c, P, L, rg)) break;
+        if (pair_plane<PAIR, TX, NP, 2>(i + 2, c, P, L, rg)) break;
+        if (pair_plane<PAIR, TX, NP, 3>(i + 3, c, P, L, rg)) break;
+        if (pair_plane<PAIR, TX, NP, 4>(i + 4, c, P, L, rg)) break;
+    }
+}
+
+size_t pair_smem(int pair, int tx, int ty) {
+    return 128 + (size_t)kStages * 8 *
+                     (n_halo(pair) * round_up((tx + 4) * (ty + 4), 16) + n_tile(pair) * round_up(tx * ty, 16));
+}
+
+template <int PAIR, int TX, int NP>
+int launch_pair_tx(const PairParams &P, int nblocks, cudaStream_t st) {
+    auto fn = rkpair_kernel<PAIR, TX, NP>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(rkpair)");
+        configured = true;
+    }
+    fn<<<nblocks, (TX / NP) * P.ty, pair_smem(PAIR, TX, P.ty), st>>>(P);
+    return check_cuda(cudaGetLastError(), "rkpair_kernel launch");
+}
+
+template <int PAIR, int NP>
+int launch_pair_np(const PairParams &P, int tx, int nblocks, cudaStream_t st) {
+    switch (tx) {
+        case 32: return launch_pair_tx<PAIR, 32, NP>(P, nblocks, st);
+        case 64: return launch_pair_tx<PAIR, 64, NP>(P, nblocks, st);
+        case 128: return launch_pair_tx<PAIR, 128, NP>(P, nblocks, st);
+        default: return fail(SB_USAGE, "tile_x must be 32, 64 or 128");
+    }
+}
+
+}  // namespace
+
+int launch_rk4_pair(int pair, const sb_array *halo, int nh, const sb_array *tile, int nt, const sb_array *out, int no,
+                    const sb_space &sp, const sb_rk4_constants &k, const sb_launch &p, cudaStream_t st) {
+    const int TX = p.tile_x, TY = p.tile_y, ZC = p.z_chunk;
+    const int NP = (p.flags & SB_LAUNCH_SCALAR) ? 1 : 2;
+    if (TX != 32 && TX != 64 && TX != 128) return fail(SB_USAGE, "tile_x must be 32, 64 or 128");
+    if (TY < 1 || ZC < 1) return fail(SB_USAGE, "tile_y and z_chunk must be positive");
+    const int threads = (TX / NP) * TY;
+    if (threads % 32 || threads > max_threads_pair(NP))
+        return fail(SB_USAGE, "threads per CTA must be a multiple of 32 and <= 256 (pairs) / 512 (scalar)");
+    if (TY + 4 > 256) return fail(SB_USAGE, "tile_y + 4 exceeds the TMA box limit of 256");
+    if (pair_smem(pair, TX, TY) > 227 * 1024) return fail(SB_RESOURCE, "tile needs more than 227 KB of shared memory");
+    for (int d = 0; d < 3; ++d)
+        if (sp.hi[d] <= sp.lo[d]) return SB_OK;
+    for (int a = 1; a < no; ++a)
+        if (out[a].sy != out[0].sy || out[a].sz != out[0].sz)
+            return fail(SB_USAGE, "rk4_pair: outputs must share row and plane strides");
+
+    PairParams P;
+    memset(&P, 0, sizeof(P));
+    for (int h = 0; h < nh; ++h) {
+        int rc = make_tmap(&P.hmap[h], halo[h], TX + 4, TY + 4, 1);
+        if (rc) return rc;
+        P.htma0[h][0] = halo[h].xpad;
+        P.htma0[h][1] = halo[h].ghost;
+        P.htma0[h][2] = halo[h].ghost;
+    }
+    for (int t = 0; t < nt; ++t) {
+        int rc = make_tmap(&P.tmap[t], tile[t], TX, TY, 1);
+        if (rc) return rc;
+        P.ttma0[t][0] = tile[t].xpad;
+        P.ttma0[t][1] = tile[t].ghost;
+        P.ttma0[t][2] = tile[t].ghost;
+    }
+    for (int a = 0; a < no; ++a) P.out[a] = out[a].origin;
+    P.sy = out[0].sy;
+    P.sz = out[0].sz;
+    for (int d = 0; d < 3; ++d) {
+        P.lo[d] = sp.lo[d];
+        P.hi[d] = sp.hi[d];
+    }
+    P.ax0 = (sp.lo[0] >= 0 ? sp.lo[0] / TX : -((-sp.lo[0] + TX - 1) / TX)) * TX;
+    P.ntx = (sp.hi[0] - P.ax0 + TX - 1) / TX;
+    P.nty = (sp.hi[1] - sp.lo[1] + TY - 1) / TY;
+    const int ntz = (sp.hi[2] - sp.lo[2] + ZC - 1) / ZC;
+    P.ty = TY;
+    P.zc = ZC;
+    P.k2 = k.lap.k2;
+    P.hdt = k.half_dt;
+    P.dt = k.dt;
+    P.dt6 = k.dt6;
+    if (p.flags & SB_LAUNCH_PERIODIC_GHOSTS) {
+        const sb_array &O = out[0];
+        if (O.ghost < 1 || O.ghost > O.nx || O.ghost > O.ny || O.ghost > O.nz)
+            return fail(SB_USAGE, "periodic ghost refresh needs 1 <= ghost <= every extent");
+        for (int d = 0; d < 3; ++d)
+            if (sp.lo[d] != 0 || sp.hi[d] != (d == 0 ? O.nx : d == 1 ? O.ny : O.nz))
+                return fail(SB_USAGE, "periodic ghost refresh needs the sweep to cover the whole interior");
+        if (out[1].ghost != O.ghost || out[1].nx != O.nx || out[1].ny != O.ny || out[1].nz != O.nz)
+            return fail(SB_USAGE, "periodic ghost refresh: phi and pi outputs must share geometry");
+        P.per[0] = O.nx;
+        P.per[1] = O.ny;
+        P.per[2] = O.nz;
+        P.pghost = O.ghost;
+    }
+    const long long nb = (long long)P.ntx * P.nty * ntz;
+    if (nb > 0x7fffffffLL) return fail(SB_RESOURCE, "too many tiles for one launch");
+    if (pair == 0)
+        return NP == 1 ? launch_pair_np<PAIR_A, 1>(P, TX, (int)nb, st) : launch_pair_np<PAIR_A, 2>(P, TX, (int)nb, st);
+    return NP == 1 ? launch_pair_np<PAIR_B, 1>(P, TX, (int)nb, st) : launch_pair_np<PAIR_B, 2>(P, TX, (int)nb, st);
+}
+
+}  // namespace sb

@@ -272,24 +272,38 @@ class PeriodicGhosts:
 
 
 class WaveRK4:
-    """K5 — one classical RK4 step of d/dt(phi, pi) = (pi, Lap4 phi) on a
-    periodic box: four stage launches.  Each stage also refreshes the ghost
-    shell of the phi it produces (fused periodic refill), so after the
-    initial fill of phi0 no separate ghost kernel runs; ``fused_ghosts=False``
-    uses the stand-alone K4 refill before every stage instead.  State
-    buffers are allocated once."""
+    """One classical RK4 step of d/dt(phi, pi) = (pi, Lap4 phi) on a periodic
+    box.  ``schedule``:
+
+    * ``"pairs"`` (default) — K5b, two launches per step with the stages
+      fused in pairs (temporal blocking, 14 array passes);
+    * ``"stages"`` — K5, four stage launches (32 passes);
+    * ``"stages_unfused"`` — four stage launches each preceded by the
+      stand-alone K4 periodic ghost refill.
+
+    Every schedule gives the same bits.  The fused schedules refresh the
+    periodic ghost shells of the phi (and, for pairs, pi) they produce, so
+    after :meth:`fill_ghosts` of the initial state no ghost pass runs."""
 
     site_id = "wave_rk4"
+    SCHEDULES = ("pairs", "stages", "stages_unfused")
 
-    def __init__(self, n: int, ghost: int, c: WaveConstants, device=None, fused_ghosts: bool = True):
+    def __init__(self, n: int, ghost: int, c: WaveConstants, device=None, schedule: str = "pairs"):
+        if schedule not in self.SCHEDULES:
+            raise UsageError(f"unknown RK4 schedule {schedule!r}")
         self.n, self.g, self.c = n, ghost, c
-        self.fused_ghosts = fused_ghosts
+        self.schedule = schedule
         mk = lambda: DeviceGrid((n, n, n), ghost, device)
         self.phi0, self.pi0 = mk(), mk()
         self.phi_a, self.pi_a, self.phi_b, self.pi_b = mk(), mk(), mk(), mk()
         self.acc_phi, self.acc_pi = mk(), mk()
-        # best of the sweep at 384^3 (profiles/r01/v3_sweep_c3_tma_pointwise_fused_ghosts.jsonl)
-        self.params = LaunchParams(64, 4, 16, 1)   # v4 A/B: profiles/r01/v4_c3_rk2_ab.log
+        # best of the sweeps at 384^3: pairs profiles/r01/v6_sweep_c3_pairs.jsonl,
+        # stages profiles/r01/v4_c3_rk2_ab.log
+        self.params = LaunchParams(32, 4, 32, 2) if schedule == "pairs" else LaunchParams(64, 4, 16, 1)
+
+    @property
+    def fused_ghosts(self) -> bool:
+        return self.schedule != "stages_unfused"
 
     def launch_space(self) -> LaunchSpace:
         return RK4_SPACE
@@ -300,22 +314,37 @@ class WaveRK4:
     def fill_ghosts(self, grid: DeviceGrid, stream=None) -> None:
         _lib.call("sb_ghost_periodic", grid.abi(), stream_ptr(stream))
 
+    def _fields(self, phi_s, pi_s, phi_out, pi_out) -> _lib.sb_rk4_fields:
+        return _lib.sb_rk4_fields(phi_s.abi(), pi_s.abi(), self.phi0.abi(), self.pi0.abi(), self.acc_phi.abi(),
+                                  self.acc_pi.abi(), phi_out.abi(), pi_out.abi())
+
+    def _whole(self):
+        n = self.n
+        return _lib.space((0, 0, 0), (n, n, n))
+
     def stage(self, s: int, phi_s: DeviceGrid, pi_s: DeviceGrid, phi_out: DeviceGrid, pi_out: DeviceGrid,
               params: LaunchParams, stream=None) -> None:
         if not self.fused_ghosts:
             self.fill_ghosts(phi_s, stream)
-        f = _lib.sb_rk4_fields(phi_s.abi(), pi_s.abi(), self.phi0.abi(), self.pi0.abi(), self.acc_phi.abi(),
-                               self.acc_pi.abi(), phi_out.abi(), pi_out.abi())
-        n = self.n
+        f = self._fields(phi_s, pi_s, phi_out, pi_out)
         flags = _lib.SB_LAUNCH_PERIODIC_GHOSTS if self.fused_ghosts else 0
-        _lib.call("sb_rk4_stage", s, C.byref(f), _lib.space((0, 0, 0), (n, n, n)), self._consts(),
-                  _lib.launch_of(params, flags), stream_ptr(stream))
+        _lib.call("sb_rk4_stage", s, C.byref(f), self._whole(), self._consts(), _lib.launch_of(params, flags),
+                  stream_ptr(stream))
+
+    def pair(self, k: int, phi_s: DeviceGrid, pi_s: DeviceGrid, phi_out: DeviceGrid, pi_out: DeviceGrid,
+             params: LaunchParams, stream=None) -> None:
+        f = self._fields(phi_s, pi_s, phi_out, pi_out)
+        _lib.call("sb_rk4_pair", k, C.byref(f), self._whole(), self._consts(),
+                  _lib.launch_of(params, _lib.SB_LAUNCH_PERIODIC_GHOSTS), stream_ptr(stream))
 
     def step(self, params: LaunchParams | None = None, stream=None) -> tuple[DeviceGrid, DeviceGrid]:
-        """One RK4 step from (phi0, pi0) (phi0's ghost shell must be filled;
-        see fill_ghosts); returns the grids holding the new state, whose phi
-        ghost shell is filled when fused_ghosts is on."""
+        """One RK4 step from (phi0, pi0) (ghost shells filled); returns the grids
+        holding the new state."""
         p = params or self.params
+        if self.schedule == "pairs":
+            self.pair(1, self.phi0, self.pi0, self.phi_a, self.pi_a, p, stream)
+            self.pair(2, self.phi_a, self.pi_a, self.phi_b, self.pi_b, p, stream)
+            return self.phi_b, self.pi_b
         self.stage(1, self.phi0, self.pi0, self.phi_a, self.pi_a, p, stream)
         self.stage(2, self.phi_a, self.pi_a, self.phi_b, self.pi_b, p, stream)
         self.stage(3, self.phi_b, self.pi_b, self.phi_a, self.pi_a, p, stream)
@@ -327,6 +356,8 @@ class WaveRK4:
         phi, pi = self.step(params, stream)
         if not self.fused_ghosts:
             self.fill_ghosts(phi, stream)
+        if self.schedule != "pairs":
+            self.fill_ghosts(pi, stream)     # pi's ghosts are only refreshed by the pair schedule
         self.phi0, self.phi_b = phi, self.phi0
         self.pi0, self.pi_b = pi, self.pi0
 

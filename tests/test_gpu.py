@@ -263,14 +263,15 @@ def test_c3_small_golden(golden):
     assert bits_equal(pi, a["c3_pi1"]), first_diff(pi, a["c3_pi1"])
 
 
-@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("schedule", ["pairs", "stages", "stages_unfused"])
 @pytest.mark.parametrize("params", [(64, 4, 16, 2), (128, 2, 48, 1), (32, 8, 5, 1)])
-def test_c3_medium_vs_oracle(fused, params):
+def test_c3_medium_vs_oracle(schedule, params):
     """Interior and (fused) periodic ghost shell of phi after one RK4 step."""
     from paper_1308_1343_b200.configs import C3WaveRK4
     from paper_1308_1343_b200.tuner import LaunchParams
     n, g = 48, 2
-    p = C3WaveRK4(n=n, seed=77, fused_ghosts=fused).setup()
+    fused = schedule != "stages_unfused"
+    p = C3WaveRK4(n=n, seed=77, schedule=schedule).setup()
     p.run(LaunchParams(*params))
     phi, pi = p.outputs()
     wphi, wpi = oracle.rk4_step(p.host_phi, p.host_pi, g, p.c)
@@ -282,11 +283,12 @@ def test_c3_medium_vs_oracle(fused, params):
         assert bits_equal(full, wphi), first_diff(full, wphi)
 
 
-def test_c3_two_steps_advance():
+@pytest.mark.parametrize("schedule", ["pairs", "stages", "stages_unfused"])
+def test_c3_two_steps_advance(schedule):
     """advance() twice equals two oracle steps (ghosts carried by the fused refill)."""
     from paper_1308_1343_b200.configs import C3WaveRK4
     n, g = 24, 2
-    p = C3WaveRK4(n=n, seed=5).setup()
+    p = C3WaveRK4(n=n, seed=5, schedule=schedule).setup()
     p.rk.advance()
     p.rk.advance()
     a, b = oracle.rk4_step(p.host_phi, p.host_pi, g, p.c)
