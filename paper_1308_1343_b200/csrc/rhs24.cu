@@ -60,7 +60,7 @@ struct Rhs24Params {
     long long osy, osz;      // output strides (shared by all outputs)
     int tma0[NV][3];
     int lo[3], hi[3];
-    int ntx, nty, zc;
+    int ax0, ntx, nty, zc;   // x tiles anchored on multiples of 8: TMA boxes start 16-byte aligned
     double k1, k2, k11;
 };
 
@@ -206,12 +206,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) rhs24_kernel(const __grid_constan
     t /= P.ntx;
     const int by = t % P.nty;
     const int bz = t / P.nty;
-    c.X0 = P.lo[0] + bx * TXc;
+    c.X0 = P.ax0 + bx * TXc;
     c.Y0 = P.lo[1] + by * TYc;
     c.Z0 = P.lo[2] + bz * P.zc;
     c.Z1 = min(c.Z0 + P.zc, P.hi[2]);
     c.nplanes = c.Z1 - c.Z0 + 4;
-    c.active = (c.X0 + c.cx < P.hi[0]) && (c.Y0 + c.cy < P.hi[1]);
+    c.active = (c.X0 + c.cx >= P.lo[0]) && (c.X0 + c.cx < P.hi[0]) && (c.Y0 + c.cy < P.hi[1]);
 
     if (c.tid == 0) {
         for (int s = 0; s < NSTAGE; ++s) mbar_init(&c.full[s], 1);
@@ -296,7 +296,8 @@ int launch_rhs24(const sb_array *in, const sb_array *out, const sb_space &sp, co
         P.hi[d] = sp.hi[d];
     }
     P.zc = p.z_chunk > 0 ? p.z_chunk : 32;
-    P.ntx = (sp.hi[0] - sp.lo[0] + TXc - 1) / TXc;
+    P.ax0 = (sp.lo[0] >= 0 ? sp.lo[0] / TXc : -((-sp.lo[0] + TXc - 1) / TXc)) * TXc;
+    P.ntx = (sp.hi[0] - P.ax0 + TXc - 1) / TXc;
     P.nty = (sp.hi[1] - sp.lo[1] + TYc - 1) / TYc;
     const int ntz = (sp.hi[2] - sp.lo[2] + P.zc - 1) / P.zc;
     P.k1 = k.k1;
