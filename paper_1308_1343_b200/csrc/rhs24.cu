@@ -23,6 +23,7 @@
 // Two CTA barriers per plane.  Bound: shared-memory bandwidth (two 8-byte
 // operand loads per term per point), then the FP64 pipe.
 #include <cstring>
+#include <mutex>
 
 #include "common.cuh"
 #include "internal.h"
@@ -233,9 +234,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) rhs24_kernel(const __grid_constan
     }
 }
 
-// Content fingerprint of the last uploaded table (uploads are stream-ordered).
+// Content fingerprint of the last uploaded table (uploads are stream-ordered);
+// the host staging copy and the fingerprint are shared, so guarded.
 uint64_t g_poly_fp = 0;
 bool g_poly_valid = false;
+std::mutex g_poly_mutex;
 
 uint64_t fnv1a(const void *data, size_t n, uint64_t h) {
     const unsigned char *b = static_cast<const unsigned char *>(data);
@@ -257,6 +260,7 @@ int launch_rhs24(const sb_array *in, const sb_array *out, const sb_space &sp, co
         if (out[v].sy != out[0].sy || out[v].sz != out[0].sz)
             return fail(SB_USAGE, "rhs24: all outputs must share row and plane strides");
 
+    std::lock_guard<std::mutex> lock(g_poly_mutex);
     static PolyConst host;
     for (int o = 0; o < NV; ++o)
         for (int t = 0; t < NT; ++t) {
