@@ -170,6 +170,13 @@ SB_API int sb_lap7(sb_array dst, sb_array src, sb_space space, double c0, double
 SB_API int sb_d4_all(const sb_array *out, sb_array src, sb_space space,
               sb_d4_constants k, sb_launch p, void *stream);
 
+/* K2' — the same ten outputs with the 2nd-order centred operators:
+ * D1 = (u[+1]-u[-1]) k1, D2 = ((u[-1]+u[+1]) - 2u) k2, D_ab = d_a(d_b) k11,
+ * Lap2 = (Dxx + Dyy) + Dzz with k1 = 1/(2h), k2 = 1/h^2, k11 = 1/(4h^2).
+ * src ghost >= 2 (the kernel stages radius-2 halos). */
+SB_API int sb_d2_all(const sb_array *out, sb_array src, sb_space space,
+                     sb_d4_constants k, sb_launch p, void *stream);
+
 /* K3 — 4th-order Laplacian over up to SB_MAX_BOXES boxes of a level in one
  * launch (config 4); the device box table replaces execute_plan's block
  * queue (traverse.py:162-209). */

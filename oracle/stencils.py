@@ -114,6 +114,35 @@ def d4_all(outs, u, g, region, k) -> None:
         o[z0:z1, y0:y1, x0:x1] = v
 
 
+def derivs9_o2(u, g, region, k) -> list[np.ndarray]:
+    """2nd-order centred Dx, Dy, Dz, Dxx, Dyy, Dzz, Dxy, Dxz, Dyz:
+    D1 = (u[+1]-u[-1])*k1, D2 = ((u[-1]+u[+1]) - 2u)*k2, D_ab = d_a(d_b)*k11
+    with the inner difference b as for 4th order (x for xy/xz, y for yz)."""
+    U = _Slab(u, g, region)
+    c = U()
+    ex = lambda dz, dy: U(dz, dy, 1) - U(dz, dy, -1)
+    ey = lambda dz, dx: U(dz, 1, dx) - U(dz, -1, dx)
+    dx = ex(0, 0) * k.k1
+    dy = ey(0, 0) * k.k1
+    dz = (U(1) - U(-1)) * k.k1
+    dxx = ((U(0, 0, -1) + U(0, 0, 1)) - 2.0 * c) * k.k2
+    dyy = ((U(0, -1) + U(0, 1)) - 2.0 * c) * k.k2
+    dzz = ((U(-1) + U(1)) - 2.0 * c) * k.k2
+    dxy = (ex(0, 1) - ex(0, -1)) * k.k11
+    dxz = (ex(1, 0) - ex(-1, 0)) * k.k11
+    dyz = (ey(1, 0) - ey(-1, 0)) * k.k11
+    return [dx, dy, dz, dxx, dyy, dzz, dxy, dxz, dyz]
+
+
+def d2_all(outs, u, g, region, k) -> None:
+    """The ten outputs with 2nd-order operators; Lap2 = (Dxx + Dyy) + Dzz."""
+    x0, x1, y0, y1, z0, z1 = region
+    ds = derivs9_o2(u, g, region, k)
+    lap = (ds[3] + ds[4]) + ds[5]
+    for o, v in zip(outs, ds + [lap]):
+        o[z0:z1, y0:y1, x0:x1] = v
+
+
 def lap4(out, u, g, region, k2) -> None:
     """Configs 3/4: Lap4 = (Dxx + Dyy) + Dzz."""
     x0, x1, y0, y1, z0, z1 = region

@@ -162,20 +162,32 @@ int sb_lap7(sb_array dst, sb_array src, sb_space space, double c0, double c1, sb
     return launch_lap7(dst, src, space, c0, c1, p, as_stream(stream));
 }
 
-int sb_d4_all(const sb_array *out, sb_array src, sb_space space, sb_d4_constants k, sb_launch p, void *stream) {
+namespace {
+int all10(int mode, const char *nm, const sb_array *out, sb_array src, sb_space space, sb_d4_constants k,
+          sb_launch p, void *stream) {
     int rc;
-    if (!out) return fail(SB_USAGE, "d4_all: null output table");
-    if ((rc = check_array(src, 2, "d4_all src")) || (rc = check_space(space, src, "d4_all"))) return rc;
+    if (!out) return fail(SB_USAGE, "all outputs: null output table");
+    if ((rc = check_array(src, 2, nm)) || (rc = check_space(space, src, nm))) return rc;
     D4Job job;
     memset(&job, 0, sizeof(job));
     job.src = src;
     job.space = space;
     for (int i = 0; i < SB_N_D4_OUT; ++i) {
-        if ((rc = check_array(out[i], 0, "d4_all out")) || (rc = check_space(space, out[i], "d4_all out")))
+        if ((rc = check_array(out[i], 0, nm)) || (rc = check_space(space, out[i], nm)))
             return rc;
         job.g[i] = out[i];
     }
-    return launch_d4(D4_ALL10, &job, 1, k, 0.0, p, as_stream(stream));
+    return launch_d4(mode, &job, 1, k, 0.0, p, as_stream(stream));
+}
+
+}  // namespace
+
+int sb_d4_all(const sb_array *out, sb_array src, sb_space space, sb_d4_constants k, sb_launch p, void *stream) {
+    return all10(D4_ALL10, "d4_all", out, src, space, k, p, stream);
+}
+
+int sb_d2_all(const sb_array *out, sb_array src, sb_space space, sb_d4_constants k, sb_launch p, void *stream) {
+    return all10(D2_ALL10, "d2_all", out, src, space, k, p, stream);
 }
 
 int sb_lap4_boxes(const sb_box_job *jobs, int32_t njobs, sb_d4_constants k, sb_launch p, void *stream) {

@@ -41,6 +41,22 @@ using namespace ops;
 constexpr int kStages = 4;
 
 // consumer threads per CTA allowed for (mode, points per thread)
+__host__ __device__ constexpr bool all10(int mode) { return mode == D4_ALL10 || mode == D2_ALL10; }
+
+// Unscaled first difference and scaled second difference of the mode's order:
+// 4th: (u[-2]-u[+2]) + 8(u[+1]-u[-1]),  ((16(u[-1]+u[+1]) - (u[-2]+u[+2])) - 30u) k2
+// 2nd: u[+1]-u[-1],                     ((u[-1]+u[+1]) - 2u) k2
+template <int MODE>
+__device__ __forceinline__ double dfirst(double m2, double m1, double p1, double p2) {
+    if constexpr (MODE == D2_ALL10) return sub(p1, m1);
+    else return d1u(m2, m1, p1, p2);
+}
+template <int MODE>
+__device__ __forceinline__ double dsecond(double m2, double m1, double c, double p1, double p2, double k2) {
+    if constexpr (MODE == D2_ALL10) return mul(sub(add(m1, p1), mul(2.0, c)), k2);
+    else return d2(m2, m1, c, p1, p2, k2);
+}
+
 __host__ __device__ constexpr int max_threads(int mode, int np) {
     return (np == 2 && mode != D4_LAP4) ? 256 : 512;
 }
@@ -49,7 +65,7 @@ __host__ __device__ constexpr int max_threads(int mode, int np) {
 #ifndef SB_D4_ALL10_MINB
 #define SB_D4_ALL10_MINB 1
 #endif
-__host__ __device__ constexpr int min_blocks(int mode) { return mode == D4_ALL10 ? SB_D4_ALL10_MINB : 1; }
+__host__ __device__ constexpr int min_blocks(int mode) { return all10(mode) ? SB_D4_ALL10_MINB : 1; }
 
 struct BoxDesc {
     CUtensorMap tmap;          // plane boxes of (TX+4) x (TY+4) x 1 over the source grid
@@ -162,7 +178,7 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
 
     double rx[NP], ryv[NP];
     double *rxs = c.rxb + (i & 1) * c.H * TX;
-    if constexpr (MODE == D4_ALL10) {
+    if constexpr (all10(MODE)) {
         // unscaled x differences of this thread's share of the 4 halo rows
         for (int h = c.ry; h < 4; h += c.TY) {
             const int hr = h < 2 ? h : c.TY + h;
@@ -170,7 +186,7 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
             row_vals<NP>(pl + hr * W + NP * c.cx, hv);
             double r[NP];
 #pragma unroll
-            for (int j = 0; j < NP; ++j) r[j] = d1u(hv[j], hv[j + 1], hv[j + 3], hv[j + 4]);
+            for (int j = 0; j < NP; ++j) r[j] = dfirst<MODE>(hv[j], hv[j + 1], hv[j + 3], hv[j + 4]);
             if constexpr (NP == 2)
                 *reinterpret_cast<double2 *>(rxs + hr * TX + 2 * c.cx) = make_double2(r[0], r[1]);
             else
@@ -178,8 +194,8 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
         }
 #pragma unroll
         for (int j = 0; j < NP; ++j) {
-            rx[j] = d1u(xr[j], xr[j + 1], xr[j + 3], xr[j + 4]);
-            ryv[j] = d1u(ym2[j], ym1[j], yp1[j], yp2[j]);
+            rx[j] = dfirst<MODE>(xr[j], xr[j + 1], xr[j + 3], xr[j + 4]);
+            ryv[j] = dfirst<MODE>(ym2[j], ym1[j], yp1[j], yp2[j]);
         }
         if constexpr (NP == 2)
             *reinterpret_cast<double2 *>(rxs + (c.ry + 2) * TX + 2 * c.cx) = make_double2(rx[0], rx[1]);
@@ -189,11 +205,11 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
     double dxx[NP], dyy[NP];
 #pragma unroll
     for (int j = 0; j < NP; ++j) {
-        dxx[j] = d2(xr[j], xr[j + 1], xr[j + 2], xr[j + 3], xr[j + 4], P.k2);
-        dyy[j] = d2(ym2[j], ym1[j], xr[j + 2], yp1[j], yp2[j], P.k2);
+        dxx[j] = dsecond<MODE>(xr[j], xr[j + 1], xr[j + 2], xr[j + 3], xr[j + 4], P.k2);
+        dyy[j] = dsecond<MODE>(ym2[j], ym1[j], xr[j + 2], yp1[j], yp2[j], P.k2);
         rg.u[R][j] = xr[j + 2];
         rg.s[R][j] = add(dxx[j], dyy[j]);
-        if constexpr (MODE == D4_ALL10) {
+        if constexpr (all10(MODE)) {
             rg.rx[R][j] = rx[j];
             rg.ry[R][j] = ryv[j];
         }
@@ -203,7 +219,7 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
     named_bar(1, c.nthr);
     if (c.tid == 0 && i + kStages < c.nplanes) issue_plane<MODE, TX>(c, P, B, i + kStages, s);
 
-    if constexpr (MODE == D4_ALL10) {
+    if constexpr (all10(MODE)) {
         if (z >= c.Z0 && z < c.Z1) {
             double r_m2[NP], r_m1[NP], r_p1[NP], r_p2[NP];
             const double *rc = rxs + NP * c.cx;
@@ -222,7 +238,7 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
             store<NP>(B.g[3] + off, dxx, L);
             store<NP>(B.g[4] + off, dyy, L);
 #pragma unroll
-            for (int j = 0; j < NP; ++j) o[j] = mul(d1u(r_m2[j], r_m1[j], r_p1[j], r_p2[j]), P.k11);
+            for (int j = 0; j < NP; ++j) o[j] = mul(dfirst<MODE>(r_m2[j], r_m1[j], r_p1[j], r_p2[j]), P.k11);
             store<NP>(B.g[6] + off, o, L);
         }
     }
@@ -234,20 +250,20 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
     double dzz[NP], lap[NP];
 #pragma unroll
     for (int j = 0; j < NP; ++j) {
-        dzz[j] = d2(rg.u[K0][j], rg.u[K1][j], rg.u[K2][j], rg.u[K3][j], rg.u[K4][j], P.k2);
+        dzz[j] = dsecond<MODE>(rg.u[K0][j], rg.u[K1][j], rg.u[K2][j], rg.u[K3][j], rg.u[K4][j], P.k2);
         lap[j] = add(rg.s[K2][j], dzz[j]);
     }
-    if constexpr (MODE == D4_ALL10) {
+    if constexpr (all10(MODE)) {
         double o[NP];
 #pragma unroll
-        for (int j = 0; j < NP; ++j) o[j] = mul(d1u(rg.u[K0][j], rg.u[K1][j], rg.u[K3][j], rg.u[K4][j]), P.k1);
+        for (int j = 0; j < NP; ++j) o[j] = mul(dfirst<MODE>(rg.u[K0][j], rg.u[K1][j], rg.u[K3][j], rg.u[K4][j]), P.k1);
         store<NP>(B.g[2] + offc, o, L);
         store<NP>(B.g[5] + offc, dzz, L);
 #pragma unroll
-        for (int j = 0; j < NP; ++j) o[j] = mul(d1u(rg.rx[K0][j], rg.rx[K1][j], rg.rx[K3][j], rg.rx[K4][j]), P.k11);
+        for (int j = 0; j < NP; ++j) o[j] = mul(dfirst<MODE>(rg.rx[K0][j], rg.rx[K1][j], rg.rx[K3][j], rg.rx[K4][j]), P.k11);
         store<NP>(B.g[7] + offc, o, L);
 #pragma unroll
-        for (int j = 0; j < NP; ++j) o[j] = mul(d1u(rg.ry[K0][j], rg.ry[K1][j], rg.ry[K3][j], rg.ry[K4][j]), P.k11);
+        for (int j = 0; j < NP; ++j) o[j] = mul(dfirst<MODE>(rg.ry[K0][j], rg.ry[K1][j], rg.ry[K3][j], rg.ry[K4][j]), P.k11);
         store<NP>(B.g[8] + offc, o, L);
         store<NP>(B.g[9] + offc, lap, L);
     } else if constexpr (MODE == D4_LAP4) {
@@ -389,7 +405,7 @@ size_t smem_bytes(int mode, int tx, int ty) {
     const int H = ty + 4;
     const int stage = round_up((tx + 4) * H, 16) + n_pointwise(mode) * round_up(tx * ty, 16);
     size_t smem = 128 + (size_t)kStages * stage * 8;
-    if (mode == D4_ALL10) smem += (size_t)2 * H * tx * 8;
+    if (all10(mode)) smem += (size_t)2 * H * tx * 8;
     return smem;
 }
 
@@ -442,7 +458,7 @@ int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, 
                               "within the mode's limit (256 for paired d4_all / RK stages, else 512)");
     if (TY + 4 > 256) return fail(SB_USAGE, "tile_y + 4 exceeds the TMA box limit of 256");
     if (smem_bytes(mode, TX, TY) > 227 * 1024) return fail(SB_RESOURCE, "tile needs more than 227 KB of shared memory");
-    const int nused = mode == D4_ALL10 ? 10 : mode == D4_LAP4 ? 1 : mode == D4_RK1 ? 5 : mode == D4_RK2 ? 8 : 9;
+    const int nused = all10(mode) ? 10 : mode == D4_LAP4 ? 1 : mode == D4_RK1 ? 5 : mode == D4_RK2 ? 8 : 9;
 
     D4Params P;
     memset(&P, 0, sizeof(P));
@@ -525,6 +541,7 @@ int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, 
     const int nb = (int)total;
     switch (mode) {
         case D4_ALL10: return launch_np<D4_ALL10>(P, TX, NP, nb, st);
+        case D2_ALL10: return launch_np<D2_ALL10>(P, TX, NP, nb, st);
         case D4_LAP4: return launch_np<D4_LAP4>(P, TX, NP, nb, st);
         case D4_RK1: return launch_np<D4_RK1>(P, TX, NP, nb, st);
         case D4_RK23: return launch_np<D4_RK23>(P, TX, NP, nb, st);

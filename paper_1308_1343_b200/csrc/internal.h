@@ -26,7 +26,8 @@ int launch_diff1d(int kind, double *dst, const double *src, int n, cudaStream_t 
 
 // RK stages: RK1 = stage 1, RK2 = stage 2 (acc_phi = pi0 + 2 pi_s: stage 1 never
 // materialises acc_phi = pi0), RK23 = stage 3, RK4 = stage 4.
-enum D4Mode { D4_ALL10 = 0, D4_LAP4 = 1, D4_RK1 = 2, D4_RK23 = 3, D4_RK4 = 4, D4_RK2 = 5 };
+// D2_ALL10: the same ten outputs with the 2nd-order centred operators.
+enum D4Mode { D4_ALL10 = 0, D4_LAP4 = 1, D4_RK1 = 2, D4_RK23 = 3, D4_RK4 = 4, D4_RK2 = 5, D2_ALL10 = 6 };
 
 struct D4Job {
     sb_array src;         // stencil input (ghost >= 2)

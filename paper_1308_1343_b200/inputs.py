@@ -69,6 +69,18 @@ class D4Constants:
         return D4Constants(1.0 / (12.0 * h), 1.0 / (12.0 * h * h), 1.0 / (144.0 * h * h))
 
 
+@dataclass(frozen=True)
+class D2Constants:
+    """2nd-order centred constants: k1 = 1/(2h), k2 = 1/h^2, k11 = 1/(4h^2)."""
+    k1: float
+    k2: float
+    k11: float
+
+    @staticmethod
+    def for_spacing(h: float) -> "D2Constants":
+        return D2Constants(1.0 / (2.0 * h), 1.0 / (h * h), 1.0 / (4.0 * h * h))
+
+
 # -- C2: 10 derivative outputs on a 256^3 box, ghost 2 ------------------------
 
 def c2_field(n: int = 256, g: int = 2, seed: int | None = None) -> np.ndarray:

@@ -153,6 +153,17 @@ class FourthOrderAll(DeviceKernel):
         cur.wait_stream(down)
 
 
+class SecondOrderAll(FourthOrderAll):
+    """K2' — the ten outputs with the 2nd-order centred operators
+    (constants: inputs.D2Constants)."""
+
+    site_id = "d2_all"
+
+    def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
+        _lib.call("sb_d2_all", self._out_abi, self.src.abi(), _local(space, self.src), _lib.d4_constants(self.k),
+                  _lib.launch_of(params), stream_ptr(stream))
+
+
 class Laplacian4(DeviceKernel):
     """K3 — 4th-order Laplacian of one box; see :class:`LevelLaplacian4` for levels."""
 

@@ -164,6 +164,46 @@ def golden_c2(n=8, g=2):
     return u, sweep(run, u.shape, g)
 
 
+def slots_o2(G: LaneGrid, z, y, i, k):
+    """2nd-order: value + 9 derivatives (d = u[+1] - u[-1], D2 = ((u[-1]+u[+1]) - 2u) k2)."""
+    L = lambda dz, dy, dx: G.load(z + dz, y + dy, i, dx)
+    ex = lambda dz, dy: sub(L(dz, dy, 1), L(dz, dy, -1))
+    ey = lambda dz, dx: sub(L(dz, 1, dx), L(dz, -1, dx))
+    sec = lambda m, cc, p: mul(sub(add(m, p), mul(c(2.0), cc)), c(k.k2))
+    cc = L(0, 0, 0)
+    return [
+        cc,
+        mul(ex(0, 0), c(k.k1)),
+        mul(ey(0, 0), c(k.k1)),
+        mul(sub(L(1, 0, 0), L(-1, 0, 0)), c(k.k1)),
+        sec(L(0, 0, -1), cc, L(0, 0, 1)),
+        sec(L(0, -1, 0), cc, L(0, 1, 0)),
+        sec(L(-1, 0, 0), cc, L(1, 0, 0)),
+        mul(sub(ex(0, 1), ex(0, -1)), c(k.k11)),
+        mul(sub(ex(1, 0), ex(-1, 0)), c(k.k11)),
+        mul(sub(ey(1, 0), ey(-1, 0)), c(k.k11)),
+    ]
+
+
+def golden_c2_order2(n=8, g=2):
+    u = inputs.c2_field(n, g, seed=inputs.seed_for(2) + 2000)
+    k = inputs.D2Constants.for_spacing(1.0 / n)
+    G = LaneGrid(u)
+
+    def run(execute):
+        outs = [blank(u.shape) for _ in range(10)]
+
+        def kern(piece):
+            for z, y, i, m in rows_of(piece):
+                s = slots_o2(G, z, y, i, k)
+                vals = s[1:] + [add(add(s[4], s[5]), s[6])]
+                for o, v in zip(outs, vals):
+                    vl.vstore_partial(o.rows[(z, y)], i, v, m)
+        execute(kern)
+        return [strip(o.to_numpy(), g) for o in outs]
+    return u, sweep(run, u.shape, g, n_settings=2)
+
+
 # -- config 4 (and the Lap4 operator of config 3) ---------------------------------
 
 def lap4_lanes(G, z, y, i, k2):
@@ -359,6 +399,11 @@ def main():
     arrays["c2_in"] = u2
     arrays["c2_out"] = np.stack(outs2)
     meta["c2"] = {"n": 8, "g": 2, "seed": inputs.seed_for(2) + 1000}
+
+    u2b, outs2b = golden_c2_order2()
+    arrays["c2o2_in"] = u2b
+    arrays["c2o2_out"] = np.stack(outs2b)
+    meta["c2_order2"] = {"n": 8, "g": 2, "seed": inputs.seed_for(2) + 2000}
 
     phi0, pi0, phin, pin = golden_c3()
     arrays["c3_phi0"], arrays["c3_pi0"], arrays["c3_phi1"], arrays["c3_pi1"] = phi0, pi0, phin, pin

@@ -416,3 +416,29 @@ def test_c2_host_pipeline_matches_device_run(chunk):
     for w, h in zip(want, h_out):
         assert bits_equal(h.numpy(), w)
     assert bits_equal(p.src.download(with_ghosts=True), p.host_u)
+
+
+def test_d2_all_golden_and_oracle(golden):
+    """2nd-order ten-output sweep: reference-vlanes golden (n=8) and the
+    oracle at n=40 on several launch shapes, sub-space included."""
+    from paper_1308_1343_b200.grid import DeviceGrid
+    from paper_1308_1343_b200.kernels import SecondOrderAll
+    from paper_1308_1343_b200.traverse import IndexSpace
+    from paper_1308_1343_b200.tuner import LaunchParams
+    meta, a = golden
+    m = meta["c2_order2"]
+    for n, u, want_all in ((m["n"], a["c2o2_in"], None), (40, inputs.c2_field(40, 2, seed=44), None)):
+        k = inputs.D2Constants.for_spacing(1.0 / n)
+        src = DeviceGrid((n,) * 3, 2)
+        src.upload(u)
+        outs = [DeviceGrid((n,) * 3, 0).fill_(0.5) for _ in range(10)]
+        kern = SecondOrderAll(outs, src, k)
+        for params in [(32, 4, 4, 2), (64, 2, 7, 1)]:
+            kern.launch(IndexSpace((0, 0, 0), (n, n, n)), LaunchParams(*params))
+            want = [np.empty((n, n, n)) for _ in range(10)]
+            oracle.d2_all(want, u, 2, (0, n, 0, n, 0, n), k)
+            for i in range(10):
+                got = outs[i].download()
+                assert bits_equal(got, want[i]), (n, params, i, first_diff(got, want[i]))
+                if n == m["n"]:
+                    assert bits_equal(got, a["c2o2_out"][i])
