@@ -41,6 +41,9 @@ enum { PAIR_A = 0, PAIR_B = 1 };
 __host__ __device__ constexpr int n_halo(int pair) { return pair == PAIR_A ? 2 : 3; }
 __host__ __device__ constexpr int n_tile(int pair) { return pair == PAIR_A ? 0 : 3; }
 __host__ __device__ constexpr int max_threads_pair(int np) { return np == 2 ? 256 : 512; }
+#ifndef SB_RKPAIR_MINB
+#define SB_RKPAIR_MINB 1
+#endif
 
 struct PairParams {
     CUtensorMap hmap[3];       // (TX+4) x (TY+4) x 1 boxes: A: phi0, pi0   B: phi3, phi0, pi3
@@ -243,7 +246,7 @@ __device__ __forceinline__ bool pair_plane(int i, const PCtx &c, const PairParam
 }
 
 template <int PAIR, int TX, int NP>
-__global__ void __launch_bounds__(max_threads_pair(NP), 1) rkpair_kernel(const __grid_constant__ PairParams P) {
+__global__ void __launch_bounds__(max_threads_pair(NP), SB_RKPAIR_MINB) rkpair_kernel(const __grid_constant__ PairParams P) {
     constexpr int TPR = TX / NP;
     constexpr int W = TX + 4;
     extern __shared__ __align__(1024) unsigned char smem[];

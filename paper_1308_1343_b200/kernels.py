@@ -308,9 +308,9 @@ class WaveRK4:
         self.phi0, self.pi0 = mk(), mk()
         self.phi_a, self.pi_a, self.phi_b, self.pi_b = mk(), mk(), mk(), mk()
         self.acc_phi, self.acc_pi = mk(), mk()
-        # best of the sweeps at 384^3: pairs profiles/r01/v6_sweep_c3_pairs.jsonl,
+        # best of the sweeps at 384^3: pairs profiles/r01/v8_rkpair_minblocks_ab.log,
         # stages profiles/r01/v4_c3_rk2_ab.log
-        self.params = LaunchParams(32, 4, 32, 2) if schedule == "pairs" else LaunchParams(64, 4, 16, 1)
+        self.params = LaunchParams(32, 4, 32, 1) if schedule == "pairs" else LaunchParams(64, 4, 16, 1)
 
     @property
     def fused_ghosts(self) -> bool:
