@@ -198,7 +198,12 @@ SB_API int sb_rk4_stage(int32_t stage, const sb_rk4_fields *f, sb_space space,
  *   pi0, acc_phi, acc_pi, writes phi_out = phi', pi_out = pi'.
  * Bit-identical to the four sb_rk4_stage launches; 14 array passes instead
  * of 32.  With SB_LAUNCH_PERIODIC_GHOSTS both phi_out and pi_out get their
- * periodic ghost shells refreshed (pi's ghosts feed the next pair). */
+ * periodic ghost shells refreshed (pi's ghosts feed the next pair).
+ * Laplacian pairs (10 array passes, same bits):
+ * pair 3 = stages 1+2: reads phi0, pi0 (ghosts valid), writes phi_out = L1 =
+ *   Lap4(phi0), pi_out = L2 = Lap4(phi0 + (dt/2) pi0);
+ * pair 4 = stages 3+4: reads phi0, pi0, phi_s = L1, pi_s = L2 (ghosts valid),
+ *   writes phi_out = phi', pi_out = pi' (acc_phi / acc_pi unused). */
 SB_API int sb_rk4_pair(int32_t pair, const sb_rk4_fields *f, sb_space space, sb_rk4_constants c, sb_launch p,
                        void *stream);
 

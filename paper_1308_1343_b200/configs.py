@@ -108,7 +108,7 @@ class C3WaveRK4:
 
     name = "c3_wave_rk4"
 
-    def __init__(self, n: int = 384, seed: int | None = None, g: int = 2, schedule: str = "pairs"):
+    def __init__(self, n: int = 384, seed: int | None = None, g: int = 2, schedule: str = "lap_pairs"):
         self.n, self.g = n, g
         self.schedule = schedule
         self.host_phi, self.host_pi = inputs.c3_fields(n, g, seed)
@@ -121,7 +121,10 @@ class C3WaveRK4:
         # writes phi3, pi3, acc_phi, acc_pi; pair 2 reads phi3, phi0, pi3
         # (ghosted), pi0, acc_phi, acc_pi and writes phi', pi'.
         shell = _vol((n,) * 3, g) - n ** 3
-        passes, ghosted = {"pairs": (14, 5), "stages": (32, 4), "stages_unfused": (32, 4)}[schedule]
+        # lap_pairs: pair 1 reads phi0, pi0 (ghosted), writes L1, L2; pair 2
+        # reads phi0, pi0, L1, L2 (ghosted) and writes phi', pi'.
+        passes, ghosted = {"pairs": (14, 5), "lap_pairs": (10, 6), "stages": (32, 4),
+                           "stages_unfused": (32, 4)}[schedule]
         self.canonical_bytes = 8 * (passes * n ** 3 + ghosted * shell)
         self.survey_canonical_bytes = 8 * (34 * n ** 3 + 4 * shell)
         self.ghost_fill_bytes = 8 * 4 * 2 * (_vol((n,) * 3, g) - n ** 3)

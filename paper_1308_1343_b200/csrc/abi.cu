@@ -270,10 +270,29 @@ int sb_rk4_stage_zslab(int32_t stage, const sb_rk4_fields *f, sb_space space, sb
 int sb_rk4_pair(int32_t pair, const sb_rk4_fields *f, sb_space space, sb_rk4_constants c, sb_launch p,
                 void *stream) {
     if (!f) return fail(SB_USAGE, "rk4_pair: null fields");
-    if (pair != 1 && pair != 2) return fail(SB_USAGE, "rk4_pair: pair must be 1 (stages 1+2) or 2 (stages 3+4)");
-    sb_array halo[3], tile[3], out[4];
+    if (pair < 1 || pair > 4)
+        return fail(SB_USAGE, "rk4_pair: pair must be 1/2 (stages 1+2 / 3+4) or 3/4 (Laplacian pairs)");
+    sb_array halo[4], tile[3], out[4];
     int nh, nt, no;
-    if (pair == 1) {
+    if (pair == 3) {
+        halo[0] = f->phi0;
+        halo[1] = f->pi0;
+        nh = 2;
+        nt = 0;
+        out[0] = f->phi_out;   // L1
+        out[1] = f->pi_out;    // L2
+        no = 2;
+    } else if (pair == 4) {
+        halo[0] = f->phi0;
+        halo[1] = f->pi0;
+        halo[2] = f->phi_s;    // L1
+        halo[3] = f->pi_s;     // L2
+        nh = 4;
+        nt = 0;
+        out[0] = f->phi_out;
+        out[1] = f->pi_out;
+        no = 2;
+    } else if (pair == 1) {
         halo[0] = f->phi0;
         halo[1] = f->pi0;
         nh = 2;

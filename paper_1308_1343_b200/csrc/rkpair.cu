@@ -12,6 +12,17 @@
 //   pair B (stages 3+4): reads phi3, phi0, pi3 (with halo), pi0, acc_phi, acc_pi;
 //                        writes phi', pi'.
 // 14 array passes per step instead of 32 for four separate stage sweeps.
+//
+// The Laplacian pairs (PAIR_LA / PAIR_LB) go further: every stage quantity is
+// a pointwise function of phi0, pi0 and the stage Laplacians, and
+//     phi3 = phi0 + (dt/2)(pi0 + (dt/2) L1),   phi4 = phi0 + dt (pi0 + (dt/2) L2),
+// so it is enough to store L1 and L2 (with their periodic ghosts):
+//   pair LA (stages 1+2): reads phi0, pi0 (with halo); writes L1, L2;
+//   pair LB (stages 3+4): reads phi0, pi0, L1, L2 (with halo); forms phi3 and
+//                         phi4 on the stencil neighbourhood, their Laplacians
+//                         L3, L4, and writes phi', pi'.
+// 10 array passes per step; the derived values repeat the stage formulas
+// operation for operation, so the bits are again those of the stage path.
 // Every value is produced by exactly the expression tree the per-stage
 // kernels (d4.cu, mode RK1/RK2/RK23/RK4) and the oracle (oracle/stencils.py:
 // rk4_step) use — the derived phi2 / phi4 are formed in registers from the
@@ -36,20 +47,28 @@ namespace {
 using namespace ops;
 
 constexpr int kStages = 4;
-enum { PAIR_A = 0, PAIR_B = 1 };
+enum { PAIR_A = 0, PAIR_B = 1, PAIR_LA = 2, PAIR_LB = 3 };
 
-__host__ __device__ constexpr int n_halo(int pair) { return pair == PAIR_A ? 2 : 3; }
-__host__ __device__ constexpr int n_tile(int pair) { return pair == PAIR_A ? 0 : 3; }
+__host__ __device__ constexpr int n_halo(int pair) { return pair == PAIR_A || pair == PAIR_LA ? 2 : pair == PAIR_B ? 3 : 4; }
+__host__ __device__ constexpr int n_out(int pair) { return pair == PAIR_A ? 4 : 2; }
+__host__ __device__ constexpr int n_tile(int pair) { return pair == PAIR_B ? 3 : 0; }
 __host__ __device__ constexpr int max_threads_pair(int np) { return np == 2 ? 256 : 512; }
 #ifndef SB_RKPAIR_MINB
 #define SB_RKPAIR_MINB 1
 #endif
+// register cap experiments (profiles/README.md): -DSB_RKPAIR_MAXNREG=<n>
+#ifdef SB_RKPAIR_MAXNREG
+#define SB_RKPAIR_BOUNDS(np) __maxnreg__(SB_RKPAIR_MAXNREG)
+#else
+#define SB_RKPAIR_BOUNDS(np) __launch_bounds__(max_threads_pair(np), SB_RKPAIR_MINB)
+#endif
 
 struct PairParams {
-    CUtensorMap hmap[3];       // (TX+4) x (TY+4) x 1 boxes: A: phi0, pi0   B: phi3, phi0, pi3
+    CUtensorMap hmap[4];       // (TX+4) x (TY+4) x 1 boxes: A: phi0, pi0   B: phi3, phi0, pi3
+                               //                            LA: phi0, pi0  LB: phi0, pi0, L1, L2
     CUtensorMap tmap[3];       // TX x TY x 1 boxes:         B: pi0, acc_phi, acc_pi
-    int htma0[3][3], ttma0[3][3];
-    double *out[4];            // A: phi3, pi3, acc_phi, acc_pi   B: phi', pi'
+    int htma0[4][3], ttma0[3][3];
+    double *out[4];            // A: phi3, pi3, acc_phi, acc_pi   B, LB: phi', pi'   LA: L1, L2
     long long sy, sz;          // strides shared by the outputs
     int lo[3], hi[3];
     int ax0, ntx, nty, ty, zc;
@@ -63,6 +82,7 @@ struct PCtx {
     int plane_elems, tile_elems, stage_elems, H, TY, nthr, tid, cx, ry;
     int X0, Y0, Z0, Z1, nplanes;
     long long off_xy;
+    bool xy_edge;   // periodic refresh: the thread's points lie within pghost of an x or y face
 };
 
 template <int NP>
@@ -70,7 +90,9 @@ struct PRings {
     double ua[5][NP], sa[5][NP];   // A: phi0       B: phi3   (value, Dxx + Dyy)
     double ub[5][NP], sb[5][NP];   // A: phi2       B: phi4
     double c1[5][NP];              // A: pi0        B: phi0   (centre values)
-    double c2[5][NP];              //               B: pi3
+    double c2[5][NP];              //               B: pi3    LB: pi0
+    double c3[5][NP], c4[5][NP];   //                         LB: L1, L2
+    double *o[4];                  // the thread's output addresses in the current plane
 };
 
 template <int PAIR, int TX>
@@ -129,18 +151,18 @@ struct Nbhd {
     }
 };
 
+// store v at off; points within pghost of a periodic face (edge: hoisted
+// per thread in x/y, per plane in z) also write their ghost images
 template <int NP>
-__device__ __forceinline__ void out_periodic(const PairParams &P, double *base, long long off, int x, int y, int z,
-                                             const double (&v)[NP], const Lanes<NP> &L) {
-    store<NP>(base + off, v, L);
-    if (!P.per[0]) return;
-    const int g = P.pghost;
-    if (x >= g && x + NP <= P.per[0] - g && y >= g && y < P.per[1] - g && z >= g && z < P.per[2] - g) return;
+__device__ __forceinline__ void out_periodic(const PairParams &P, double *base, double *at, bool edge, int x,
+                                             int y, int z, const double (&v)[NP], const Lanes<NP> &L) {
+    store<NP>(at, v, L);
+    if (!edge) return;
 #pragma unroll
     for (int j = 0; j < NP; ++j)
         if (L.m[j])
-            store_images(base, P.sy, P.sz, P.per[0], P.per[1], P.per[2], g, base, P.per[2], base, -P.per[2], x + j,
-                         y, z, v[j]);
+            store_images(base, P.sy, P.sz, P.per[0], P.per[1], P.per[2], P.pghost, base, P.per[2], base, -P.per[2],
+                         x + j, y, z, v[j]);
 }
 
 template <int PAIR, int TX, int NP, int R>
@@ -155,7 +177,35 @@ __device__ __forceinline__ bool pair_plane(int i, const PCtx &c, const PairParam
     const double *pl = c.stages + s * c.stage_elems;
 
     double tv[3][NP];   // B: pi0, acc_phi, acc_pi at the thread's points of plane zc
-    {
+    if constexpr (PAIR == PAIR_LB) {
+        // phi3 = phi0 + (dt/2) pi2, pi2 = pi0 + (dt/2) L1;  phi4 = phi0 + dt pi3, pi3 = pi0 + (dt/2) L2
+        Nbhd<TX, NP> f0, q0, l, p, d;
+        f0.load(pl, c.ry, c.cx);
+        q0.load(pl + c.plane_elems, c.ry, c.cx);
+        l.load(pl + 2 * c.plane_elems, c.ry, c.cx);
+        double s3[NP], s4[NP];
+        p.combine(q0, P.hdt, l);
+        d.combine(f0, P.hdt, p);
+        d.lap_xy(P.k2, s3);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            rg.ua[R][j] = d.xr[j + 2];
+            rg.sa[R][j] = s3[j];
+            rg.c3[R][j] = l.xr[j + 2];
+        }
+        l.load(pl + 3 * c.plane_elems, c.ry, c.cx);
+        p.combine(q0, P.hdt, l);
+        d.combine(f0, P.dt, p);
+        d.lap_xy(P.k2, s4);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            rg.ub[R][j] = d.xr[j + 2];
+            rg.sb[R][j] = s4[j];
+            rg.c4[R][j] = l.xr[j + 2];
+            rg.c1[R][j] = f0.xr[j + 2];
+            rg.c2[R][j] = q0.xr[j + 2];
+        }
+    } else {
         Nbhd<TX, NP> a, b, d;
         a.load(pl, c.ry, c.cx);                       // A: phi0   B: phi3
         b.load(pl + c.plane_elems, c.ry, c.cx);       // A: pi0    B: phi0
@@ -172,7 +222,17 @@ __device__ __forceinline__ bool pair_plane(int i, const PCtx &c, const PairParam
                 rg.sb[R][j] = sb2[j];
                 rg.c1[R][j] = b.xr[j + 2];
             }
-        } else {
+        } else if constexpr (PAIR == PAIR_LA) {
+            d.combine(a, P.hdt, b);                   // phi2 = phi0 + (dt/2) pi0
+            d.lap_xy(P.k2, sb2);
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                rg.ua[R][j] = a.xr[j + 2];
+                rg.sa[R][j] = sa[j];
+                rg.ub[R][j] = d.xr[j + 2];
+                rg.sb[R][j] = sb2[j];
+            }
+        } else if constexpr (PAIR == PAIR_B) {
             Nbhd<TX, NP> p3;
             p3.load(pl + 2 * c.plane_elems, c.ry, c.cx);   // pi3
             d.combine(b, P.dt, p3);                   // phi4 = phi0 + dt pi3
@@ -199,8 +259,8 @@ __device__ __forceinline__ bool pair_plane(int i, const PCtx &c, const PairParam
     if (i < 4) return false;
 
     constexpr int K0 = (R + 1) % 5, K1 = (R + 2) % 5, K2 = (R + 3) % 5, K3 = (R + 4) % 5, K4 = R;
-    const long long offc = c.off_xy + (long long)zc * P.sz;
     const int x = c.X0 + NP * c.cx, y = c.Y0 + c.ry;
+    const bool edge = c.xy_edge || (P.per[0] && (zc < P.pghost || zc >= P.per[2] - P.pghost));
     double la[NP], lb[NP];
 #pragma unroll
     for (int j = 0; j < NP; ++j) {
@@ -221,10 +281,29 @@ __device__ __forceinline__ bool pair_plane(int i, const PCtx &c, const PairParam
             af[j] = add(pi0, mul(2.0, pi2));
             ap[j] = add(la[j], mul(2.0, lb[j]));
         }
-        out_periodic<NP>(P, P.out[0], offc, x, y, zc, f3, L);
-        out_periodic<NP>(P, P.out[1], offc, x, y, zc, p3, L);
-        store<NP>(P.out[2] + offc, af, L);
-        store<NP>(P.out[3] + offc, ap, L);
+        out_periodic<NP>(P, P.out[0], rg.o[0], edge, x, y, zc, f3, L);
+        out_periodic<NP>(P, P.out[1], rg.o[1], edge, x, y, zc, p3, L);
+        store<NP>(rg.o[2], af, L);
+        store<NP>(rg.o[3], ap, L);
+    } else if constexpr (PAIR == PAIR_LA) {
+        out_periodic<NP>(P, P.out[0], rg.o[0], edge, x, y, zc, la, L);   // L1 = Lap(phi0)
+        out_periodic<NP>(P, P.out[1], rg.o[1], edge, x, y, zc, lb, L);   // L2 = Lap(phi2)
+    } else if constexpr (PAIR == PAIR_LB) {
+        // la = L3, lb = L4; the stage 1-3 quantities are re-formed from phi0, pi0, L1, L2
+        double fn[NP], pn[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            const double phi0 = rg.c1[K2][j], pi0 = rg.c2[K2][j], l1 = rg.c3[K2][j], l2 = rg.c4[K2][j];
+            const double pi2 = add(pi0, mul(P.hdt, l1));
+            const double pi3 = add(pi0, mul(P.hdt, l2));
+            const double pi4 = add(pi0, mul(P.dt, la[j]));
+            const double acf = add(add(pi0, mul(2.0, pi2)), mul(2.0, pi3));
+            const double acp = add(add(l1, mul(2.0, l2)), mul(2.0, la[j]));
+            fn[j] = add(phi0, mul(P.dt6, add(acf, pi4)));
+            pn[j] = add(pi0, mul(P.dt6, add(acp, lb[j])));
+        }
+        out_periodic<NP>(P, P.out[0], rg.o[0], edge, x, y, zc, fn, L);
+        out_periodic<NP>(P, P.out[1], rg.o[1], edge, x, y, zc, pn, L);
     } else {
         // stage 3: pi4 = pi0 + dt L3, acc_phi += 2 pi3, acc_pi += 2 L3   (phi4 = phi0 + dt pi3)
         // stage 4: phi' = phi0 + (dt/6)(acc_phi + pi4), pi' = pi0 + (dt/6)(acc_pi + L4)
@@ -239,14 +318,16 @@ __device__ __forceinline__ bool pair_plane(int i, const PCtx &c, const PairParam
             fn[j] = add(phi0, mul(P.dt6, add(acf3, pi4)));
             pn[j] = add(pi0, mul(P.dt6, add(acp3, lb[j])));
         }
-        out_periodic<NP>(P, P.out[0], offc, x, y, zc, fn, L);
-        out_periodic<NP>(P, P.out[1], offc, x, y, zc, pn, L);
+        out_periodic<NP>(P, P.out[0], rg.o[0], edge, x, y, zc, fn, L);
+        out_periodic<NP>(P, P.out[1], rg.o[1], edge, x, y, zc, pn, L);
     }
+#pragma unroll
+    for (int k = 0; k < n_out(PAIR); ++k) rg.o[k] += P.sz;
     return false;
 }
 
 template <int PAIR, int TX, int NP>
-__global__ void __launch_bounds__(max_threads_pair(NP), SB_RKPAIR_MINB) rkpair_kernel(const __grid_constant__ PairParams P) {
+__global__ void SB_RKPAIR_BOUNDS(NP) rkpair_kernel(const __grid_constant__ PairParams P) {
     constexpr int TPR = TX / NP;
     constexpr int W = TX + 4;
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -279,6 +360,8 @@ __global__ void __launch_bounds__(max_threads_pair(NP), SB_RKPAIR_MINB) rkpair_k
     const bool yin = y < P.hi[1];
 #pragma unroll
     for (int j = 0; j < NP; ++j) L.m[j] = (yin && x + j >= P.lo[0] && x + j < P.hi[0]) ? 1 : 0;
+    c.xy_edge = P.per[0] && !(x >= P.pghost && x + NP <= P.per[0] - P.pghost && y >= P.pghost &&
+                              y < P.per[1] - P.pghost);
     if constexpr (NP == 2) {
         L.full = L.m[0] & L.m[1];
         L.only0 = L.m[0] & (L.m[1] ^ 1);
@@ -297,7 +380,10 @@ __global__ void __launch_bounds__(max_threads_pair(NP), SB_RKPAIR_MINB) rkpair_k
     for (int k = 0; k < 5; ++k)
 #pragma unroll
         for (int j = 0; j < NP; ++j)
-            rg.ua[k][j] = rg.sa[k][j] = rg.ub[k][j] = rg.sb[k][j] = rg.c1[k][j] = rg.c2[k][j] = 0.0;
+            rg.ua[k][j] = rg.sa[k][j] = rg.ub[k][j] = rg.sb[k][j] = rg.c1[k][j] = rg.c2[k][j] = rg.c3[k][j] =
+                rg.c4[k][j] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) rg.o[k] = P.out[k] + c.off_xy + (long long)c.Z0 * P.sz;
     for (int i = 0;; i += 5) {
         if (pair_plane<PAIR, TX, NP, 0>(i + 0, c, P, L, rg)) break;
         if (pair_plane<PAIR, TX, NP, 1>(i + 1, c, P, L, rg)) break;
@@ -403,9 +489,18 @@ int launch_rk4_pair(int pair, const sb_array *halo, int nh, const sb_array *tile
     }
     const long long nb = (long long)P.ntx * P.nty * ntz;
     if (nb > 0x7fffffffLL) return fail(SB_RESOURCE, "too many tiles for one launch");
-    if (pair == 0)
-        return NP == 1 ? launch_pair_np<PAIR_A, 1>(P, TX, (int)nb, st) : launch_pair_np<PAIR_A, 2>(P, TX, (int)nb, st);
-    return NP == 1 ? launch_pair_np<PAIR_B, 1>(P, TX, (int)nb, st) : launch_pair_np<PAIR_B, 2>(P, TX, (int)nb, st);
+    switch (pair) {
+        case PAIR_A:
+            return NP == 1 ? launch_pair_np<PAIR_A, 1>(P, TX, (int)nb, st) : launch_pair_np<PAIR_A, 2>(P, TX, (int)nb, st);
+        case PAIR_B:
+            return NP == 1 ? launch_pair_np<PAIR_B, 1>(P, TX, (int)nb, st) : launch_pair_np<PAIR_B, 2>(P, TX, (int)nb, st);
+        case PAIR_LA:
+            return NP == 1 ? launch_pair_np<PAIR_LA, 1>(P, TX, (int)nb, st)
+                           : launch_pair_np<PAIR_LA, 2>(P, TX, (int)nb, st);
+        default:
+            return NP == 1 ? launch_pair_np<PAIR_LB, 1>(P, TX, (int)nb, st)
+                           : launch_pair_np<PAIR_LB, 2>(P, TX, (int)nb, st);
+    }
 }
 
 }  // namespace sb

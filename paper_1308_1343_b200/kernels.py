@@ -286,8 +286,11 @@ class WaveRK4:
     """One classical RK4 step of d/dt(phi, pi) = (pi, Lap4 phi) on a periodic
     box.  ``schedule``:
 
-    * ``"pairs"`` (default) — K5b, two launches per step with the stages
-      fused in pairs (temporal blocking, 14 array passes);
+    * ``"lap_pairs"`` (default) — K5b, two launches per step with the
+      stages fused in pairs (temporal blocking) and only the stage
+      Laplacians L1, L2 stored between them (10 array passes);
+    * ``"pairs"`` — K5b storing phi3, pi3 and the two RK accumulators
+      between the launches (14 array passes);
     * ``"stages"`` — K5, four stage launches (32 passes);
     * ``"stages_unfused"`` — four stage launches each preceded by the
       stand-alone K4 periodic ghost refill.
@@ -297,9 +300,9 @@ class WaveRK4:
     after :meth:`fill_ghosts` of the initial state no ghost pass runs."""
 
     site_id = "wave_rk4"
-    SCHEDULES = ("pairs", "stages", "stages_unfused")
+    SCHEDULES = ("pairs", "lap_pairs", "stages", "stages_unfused")
 
-    def __init__(self, n: int, ghost: int, c: WaveConstants, device=None, schedule: str = "pairs"):
+    def __init__(self, n: int, ghost: int, c: WaveConstants, device=None, schedule: str = "lap_pairs"):
         if schedule not in self.SCHEDULES:
             raise UsageError(f"unknown RK4 schedule {schedule!r}")
         self.n, self.g, self.c = n, ghost, c
@@ -308,9 +311,9 @@ class WaveRK4:
         self.phi0, self.pi0 = mk(), mk()
         self.phi_a, self.pi_a, self.phi_b, self.pi_b = mk(), mk(), mk(), mk()
         self.acc_phi, self.acc_pi = mk(), mk()
-        # best of the sweeps at 384^3: pairs profiles/r01/v8_rkpair_minblocks_ab.log,
+        # best of the sweeps at 384^3: pairs profiles/r01/v9_c3_lap_pairs_ab.log,
         # stages profiles/r01/v4_c3_rk2_ab.log
-        self.params = LaunchParams(32, 4, 32, 1) if schedule == "pairs" else LaunchParams(64, 4, 16, 1)
+        self.params = LaunchParams(32, 4, 32, 1) if "pairs" in schedule else LaunchParams(64, 4, 16, 1)
 
     @property
     def fused_ghosts(self) -> bool:
@@ -356,6 +359,11 @@ class WaveRK4:
             self.pair(1, self.phi0, self.pi0, self.phi_a, self.pi_a, p, stream)
             self.pair(2, self.phi_a, self.pi_a, self.phi_b, self.pi_b, p, stream)
             return self.phi_b, self.pi_b
+        if self.schedule == "lap_pairs":
+            # phi_a / pi_a hold L1 / L2 between the two launches
+            self.pair(3, self.phi0, self.pi0, self.phi_a, self.pi_a, p, stream)
+            self.pair(4, self.phi_a, self.pi_a, self.phi_b, self.pi_b, p, stream)
+            return self.phi_b, self.pi_b
         self.stage(1, self.phi0, self.pi0, self.phi_a, self.pi_a, p, stream)
         self.stage(2, self.phi_a, self.pi_a, self.phi_b, self.pi_b, p, stream)
         self.stage(3, self.phi_b, self.pi_b, self.phi_a, self.pi_a, p, stream)
@@ -367,8 +375,8 @@ class WaveRK4:
         phi, pi = self.step(params, stream)
         if not self.fused_ghosts:
             self.fill_ghosts(phi, stream)
-        if self.schedule != "pairs":
-            self.fill_ghosts(pi, stream)     # pi's ghosts are only refreshed by the pair schedule
+        if "pairs" not in self.schedule:
+            self.fill_ghosts(pi, stream)     # pi's ghosts are only refreshed by the pair schedules
         self.phi0, self.phi_b = phi, self.phi0
         self.pi0, self.pi_b = pi, self.pi0
 

@@ -263,7 +263,7 @@ def test_c3_small_golden(golden):
     assert bits_equal(pi, a["c3_pi1"]), first_diff(pi, a["c3_pi1"])
 
 
-@pytest.mark.parametrize("schedule", ["pairs", "stages", "stages_unfused"])
+@pytest.mark.parametrize("schedule", ["pairs", "lap_pairs", "stages", "stages_unfused"])
 @pytest.mark.parametrize("params", [(64, 4, 16, 2), (128, 2, 48, 1), (32, 8, 5, 1)])
 def test_c3_medium_vs_oracle(schedule, params):
     """Interior and (fused) periodic ghost shell of phi after one RK4 step."""
@@ -283,7 +283,7 @@ def test_c3_medium_vs_oracle(schedule, params):
         assert bits_equal(full, wphi), first_diff(full, wphi)
 
 
-@pytest.mark.parametrize("schedule", ["pairs", "stages", "stages_unfused"])
+@pytest.mark.parametrize("schedule", ["pairs", "lap_pairs", "stages", "stages_unfused"])
 def test_c3_two_steps_advance(schedule):
     """advance() twice equals two oracle steps (ghosts carried by the fused refill)."""
     from paper_1308_1343_b200.configs import C3WaveRK4

@@ -87,7 +87,7 @@ def test_lap4_level_footprint():
         check_footprint(d, allowed_mask(d))
 
 
-@pytest.mark.parametrize("schedule", ["pairs", "stages"])
+@pytest.mark.parametrize("schedule", ["pairs", "lap_pairs", "stages"])
 def test_rk4_footprint_interior_and_shell(schedule):
     from paper_1308_1343_b200.configs import C3WaveRK4
     n = 20

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--graph", action="store_true", help="time reps launches captured in one CUDA graph")
     ap.add_argument("--flags", type=int, default=0, help="extra SB_LAUNCH_* flags for the kernel")
+    ap.add_argument("--schedule", default=None, help="config 3: RK4 schedule (kernels.WaveRK4.SCHEDULES)")
     args = ap.parse_args()
 
     import torch
@@ -35,6 +36,8 @@ def main():
 
     _build.build()
     kw = {"n": args.n} if args.n else {}
+    if args.schedule:
+        kw["schedule"] = args.schedule
     prob = CONFIGS[args.config](**kw).setup()
     kern = getattr(prob, "kernel", None)
     if kern is not None and args.flags:
