@@ -67,18 +67,21 @@ def test_offset_box_level_coordinates():
         assert same(outs[i].download(), want[i]), i
 
 
-@pytest.mark.parametrize("n", [1, 3, 30])
-def test_rk4_small_and_ragged_periodic(n):
+@pytest.mark.parametrize("schedule", ["lap_pairs", "pairs", "stages"])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 30])
+def test_rk4_small_and_ragged_periodic(n, schedule):
     from paper_1308_1343_b200.configs import C3WaveRK4
     g = 2
     if n < g:
         pytest.skip("periodic ghost width must not exceed the extent")
-    p = C3WaveRK4(n=n, seed=n).setup()
+    p = C3WaveRK4(n=n, seed=n, schedule=schedule).setup()
     p.run(LaunchParams(32, 4, 5, 1))
     wphi, wpi = oracle.rk4_step(p.host_phi, p.host_pi, g, p.c)
     assert same(p.phi_with_ghosts(), wphi)
     I = (slice(g, g + n),) * 3
     assert same(p.outputs()[1], wpi[I])
+    if "pairs" in schedule:   # the pair schedules also refresh pi's ghosts
+        assert same(p.rk.pi_b.download(with_ghosts=True), wpi)
 
 
 @pytest.mark.parametrize("n,zc", [(13, 5), (9, 192), (2, 1)])
