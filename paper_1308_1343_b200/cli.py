@@ -7,10 +7,12 @@ tuned, check the outputs are bit-identical, write the per-iteration CSV
 bit-identical, 1 otherwise, 2 on usage/resource errors (cli.py:288-295).
 The device adds a fourth implementation, ``graphed`` (the same sweeps
 captured in a CUDA graph).  ``config-bench`` times one BASELINE.json
-configuration (1..5) with the run-time tuner.
+configuration (1..5) with the run-time tuner.  ``tune-sim`` runs the
+tuner against a synthetic cost surface (reference cli.py:212-226; no GPU).
 
     python -m paper_1308_1343_b200 stencil-bench --extent 64 --iters 100 --threads 2
     python -m paper_1308_1343_b200 config-bench --config 2 --iters 50
+    python -m paper_1308_1343_b200 tune-sim --seeds 100 --iters 50 --space launch
 """
 from __future__ import annotations
 
@@ -113,6 +115,20 @@ def cmd_config_bench(args) -> int:
     return 0
 
 
+def cmd_tune_sim(args) -> int:
+    from . import tunesim
+    case = tunesim.launch_case if args.space == "launch" else tunesim.plan_case
+    topo, setup, surf, space = case()
+    if args.topology:
+        topo = TopologyConfig.from_file(args.topology)
+    r = tunesim.simulate(args.seeds, args.iters, topo, setup, surf, space)
+    print(f"tune-sim ({args.space} space): optimum {r.optimum:.4f}, {r.converged}/{args.seeds} seeds within 10% "
+          f"in <= {args.iters} evals (median {r.median_evals_to_target})")
+    if args.out:
+        Path(args.out).write_text(r.csv())
+    return 0
+
+
 def build_parser() -> argparse.ArgumentParser:
     ap = argparse.ArgumentParser(prog="paper_1308_1343_b200")
     sub = ap.add_subparsers(dest="command", required=True)
@@ -136,6 +152,13 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--tune", type=int, default=30)
     p.add_argument("--seed-config", dest="seed_config", type=int, default=None)
     p.set_defaults(fn=cmd_config_bench)
+    p = sub.add_parser("tune-sim", help="tuner simulation on a synthetic cost surface")
+    p.add_argument("--seeds", type=int, default=100)
+    p.add_argument("--iters", type=int, default=50)
+    p.add_argument("--space", choices=("plan", "launch"), default="plan")
+    p.add_argument("--topology", type=str, default=None)
+    p.add_argument("--out", type=str, default=None)
+    p.set_defaults(fn=cmd_tune_sim)
     return ap
 
 

@@ -39,3 +39,12 @@ def test_config_bench_runs(config, capsys):
     assert main(["config-bench", "--config", str(config), "--iters", "3", "--tune", "6"]) == 0
     rec = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
     assert rec["config"] == config and rec["gpts"] > 0
+
+
+def test_tune_sim(tmp_path, capsys):
+    from paper_1308_1343_b200.cli import main
+    out = tmp_path / "sim.csv"
+    assert main(["tune-sim", "--seeds", "20", "--iters", "50", "--out", str(out)]) == 0
+    assert "seeds within 10%" in capsys.readouterr().out
+    rows = out.read_text().splitlines()
+    assert rows[0] == "seed,best_cost,evals_to_within_10pct,total_cost" and len(rows) == 21
