@@ -52,6 +52,7 @@ class DeviceKernel:
 
     site_id = "kernel"
     space_kind = D4_SPACE
+    extra_flags = 0   # SB_LAUNCH_* flags added to every launch (tools/sweep.py --flags)
     default_params: LaunchParams = LaunchParams(64, 8, 32)
 
     def launch_space(self) -> LaunchSpace:
@@ -87,7 +88,7 @@ class Laplacian7(DeviceKernel):
 
     def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
         _lib.call("sb_lap7", self.dst.abi(), self.src.abi(), _local(space, self.src), self.c0, self.c1,
-                  _lib.launch_of(params), stream_ptr(stream))
+                  _lib.launch_of(params, self.extra_flags), stream_ptr(stream))
 
 
 class FourthOrderAll(DeviceKernel):
@@ -111,7 +112,7 @@ class FourthOrderAll(DeviceKernel):
 
     def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
         _lib.call("sb_d4_all", self._out_abi, self.src.abi(), _local(space, self.src), _lib.d4_constants(self.k),
-                  _lib.launch_of(params), stream_ptr(stream))
+                  _lib.launch_of(params, self.extra_flags), stream_ptr(stream))
 
     def run_host(self, host_in_ptr: int, host_out_ptrs: list[int], params: LaunchParams | None = None,
                  chunk: int = 32) -> None:
@@ -161,7 +162,7 @@ class SecondOrderAll(FourthOrderAll):
 
     def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
         _lib.call("sb_d2_all", self._out_abi, self.src.abi(), _local(space, self.src), _lib.d4_constants(self.k),
-                  _lib.launch_of(params), stream_ptr(stream))
+                  _lib.launch_of(params, self.extra_flags), stream_ptr(stream))
 
 
 class Laplacian4(DeviceKernel):
@@ -182,7 +183,7 @@ class Laplacian4(DeviceKernel):
     def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
         job = _lib.sb_box_job(self.dst.abi(), self.src.abi(), _local(space, self.src))
         _lib.call("sb_lap4_boxes", C.byref(job), 1, _lib.d4_constants(self.k),
-                  _lib.launch_of(params), stream_ptr(stream))
+                  _lib.launch_of(params, self.extra_flags), stream_ptr(stream))
 
 
 class LevelLaplacian4(DeviceKernel):
@@ -227,7 +228,7 @@ class LevelLaplacian4(DeviceKernel):
             chunk = jobs[i:i + _lib.SB_MAX_BOXES]
             arr = (_lib.sb_box_job * len(chunk))(*chunk)
             _lib.call("sb_lap4_boxes", arr, len(chunk), _lib.d4_constants(self.k),
-                      _lib.launch_of(params), stream_ptr(stream))
+                      _lib.launch_of(params, self.extra_flags), stream_ptr(stream))
 
     def launch(self, space: IndexSpace | None, params: LaunchParams, stream=None) -> None:
         self._run(self._jobs(None if space is None else space), params, stream)
@@ -409,4 +410,4 @@ class Rhs24(DeviceKernel):
     def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
         poly = _lib.sb_poly(self._coef.ctypes.data, self._p.ctypes.data, self._q.ctypes.data)
         _lib.call("sb_rhs24", self._in, self._out, _local(space, self.ins[0]), _lib.d4_constants(self.k), poly,
-                  _lib.launch_of(params), stream_ptr(stream))
+                  _lib.launch_of(params, self.extra_flags), stream_ptr(stream))
