@@ -326,13 +326,15 @@ __device__ __forceinline__ bool pair_plane(int i, const PCtx &c, const PairParam
     return false;
 }
 
-template <int PAIR, int TX, int NP>
+// TYC > 0: the tile height is a compile-time constant (the default shape),
+// so every staged-plane offset folds into an immediate; TYC = 0: P.ty
+template <int PAIR, int TX, int NP, int TYC>
 __global__ void SB_RKPAIR_BOUNDS(NP) rkpair_kernel(const __grid_constant__ PairParams P) {
     constexpr int TPR = TX / NP;
     constexpr int W = TX + 4;
     extern __shared__ __align__(1024) unsigned char smem[];
     PCtx c;
-    c.TY = P.ty;
+    c.TY = TYC > 0 ? TYC : P.ty;
     c.H = c.TY + 4;
     c.nthr = TPR * c.TY;
     c.plane_elems = round_up(W * c.H, 16);
@@ -398,9 +400,9 @@ size_t pair_smem(int pair, int tx, int ty) {
                      (n_halo(pair) * round_up((tx + 4) * (ty + 4), 16) + n_tile(pair) * round_up(tx * ty, 16));
 }
 
-template <int PAIR, int TX, int NP>
-int launch_pair_tx(const PairParams &P, int nblocks, cudaStream_t st) {
-    auto fn = rkpair_kernel<PAIR, TX, NP>;
+template <int PAIR, int TX, int NP, int TYC>
+int launch_pair_ty(const PairParams &P, int nblocks, cudaStream_t st) {
+    auto fn = rkpair_kernel<PAIR, TX, NP, TYC>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -409,6 +411,12 @@ int launch_pair_tx(const PairParams &P, int nblocks, cudaStream_t st) {
     }
     fn<<<nblocks, (TX / NP) * P.ty, pair_smem(PAIR, TX, P.ty), st>>>(P);
     return check_cuda(cudaGetLastError(), "rkpair_kernel launch");
+}
+
+template <int PAIR, int TX, int NP>
+int launch_pair_tx(const PairParams &P, int nblocks, cudaStream_t st) {
+    if (TX == 32 && NP == 1 && P.ty == 4) return launch_pair_ty<PAIR, TX, NP, 4>(P, nblocks, st);
+    return launch_pair_ty<PAIR, TX, NP, 0>(P, nblocks, st);
 }
 
 template <int PAIR, int NP>

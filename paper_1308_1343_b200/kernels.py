@@ -314,7 +314,7 @@ class WaveRK4:
         self.acc_phi, self.acc_pi = mk(), mk()
         # best of the sweeps at 384^3: pairs profiles/r01/v9_c3_lap_pairs_ab.log,
         # stages profiles/r01/v4_c3_rk2_ab.log
-        self.params = LaunchParams(32, 4, 32, 1) if "pairs" in schedule else LaunchParams(64, 4, 16, 1)
+        self.params = LaunchParams(32, 4, 64, 1) if "pairs" in schedule else LaunchParams(64, 4, 16, 1)
 
     @property
     def fused_ghosts(self) -> bool:
