@@ -327,14 +327,16 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
     return false;
 }
 
-template <int MODE, int TX, int NP>
+// TYC > 0: compile-time tile height (the default shapes), so staged-plane
+// offsets fold into immediates; TYC = 0: P.ty
+template <int MODE, int TX, int NP, int TYC>
 __global__ void __launch_bounds__(max_threads(MODE, NP), min_blocks(MODE)) d4_kernel(const __grid_constant__ D4Params P) {
     constexpr int TPR = TX / NP;    // threads per row
     constexpr int W = TX + 4;       // smem row width (elements)
     extern __shared__ __align__(1024) unsigned char smem[];
 
     Ctx c;
-    c.TY = P.ty;
+    c.TY = TYC > 0 ? TYC : P.ty;
     c.H = c.TY + 4;
     c.nthr = TPR * c.TY;
     c.plane_elems = round_up(W * c.H, 16);
@@ -409,11 +411,11 @@ size_t smem_bytes(int mode, int tx, int ty) {
     return smem;
 }
 
-template <int MODE, int TX, int NP>
-int launch_mode_tx(const D4Params &P, int nblocks, cudaStream_t st) {
+template <int MODE, int TX, int NP, int TYC>
+int launch_mode_ty(const D4Params &P, int nblocks, cudaStream_t st) {
     const int threads = (TX / NP) * P.ty;
     const size_t smem = smem_bytes(MODE, TX, P.ty);
-    auto fn = d4_kernel<MODE, TX, NP>;
+    auto fn = d4_kernel<MODE, TX, NP, TYC>;
     // raise the dynamic shared-memory limit once per instantiation (keeps the
     // launch path free of non-stream calls, e.g. during CUDA-graph capture)
     static int configured = 0;
@@ -424,6 +426,14 @@ int launch_mode_tx(const D4Params &P, int nblocks, cudaStream_t st) {
     }
     fn<<<nblocks, threads, smem, st>>>(P);
     return check_cuda(cudaGetLastError(), "d4_kernel launch");
+}
+
+template <int MODE, int TX, int NP>
+int launch_mode_tx(const D4Params &P, int nblocks, cudaStream_t st) {
+    // the swept default shapes of configs 2 and 4 (32 x 4, point pairs)
+    constexpr bool kDefault = TX == 32 && NP == 2 && (MODE == D4_ALL10 || MODE == D4_LAP4);
+    if (kDefault && P.ty == 4) return launch_mode_ty<MODE, TX, NP, 4>(P, nblocks, st);
+    return launch_mode_ty<MODE, TX, NP, 0>(P, nblocks, st);
 }
 
 template <int MODE, int NP>
