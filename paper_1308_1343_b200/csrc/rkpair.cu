@@ -56,12 +56,21 @@ __host__ __device__ constexpr int max_threads_pair(int np) { return np == 2 ? 25
 #ifndef SB_RKPAIR_MINB
 #define SB_RKPAIR_MINB 1
 #endif
-// register cap experiments (profiles/README.md): -DSB_RKPAIR_MAXNREG=<n>
-#ifdef SB_RKPAIR_MAXNREG
-#define SB_RKPAIR_BOUNDS(np) __maxnreg__(SB_RKPAIR_MAXNREG)
-#else
-#define SB_RKPAIR_BOUNDS(np) __launch_bounds__(max_threads_pair(np), SB_RKPAIR_MINB)
+// Resident CTAs the register allocation must allow for the compile-time
+// default shape (exact CTA size known): first pairs (A, LA) / second pairs
+// (B, LB).  Register-cap experiments: profiles/README.md.
+#ifndef SB_RKPAIR_MINB_FIRST
+#define SB_RKPAIR_MINB_FIRST 5
 #endif
+#ifndef SB_RKPAIR_MINB_SECOND
+#define SB_RKPAIR_MINB_SECOND 4
+#endif
+__host__ __device__ constexpr int lb_threads(int tx, int np, int tyc) {
+    return tyc > 0 ? tx / np * tyc : max_threads_pair(np);
+}
+__host__ __device__ constexpr int lb_minb(int pair, int tyc) {
+    return tyc == 0 ? SB_RKPAIR_MINB : (pair == 0 || pair == 2) ? SB_RKPAIR_MINB_FIRST : SB_RKPAIR_MINB_SECOND;
+}
 
 struct PairParams {
     CUtensorMap hmap[4];       // (TX+4) x (TY+4) x 1 boxes: A: phi0, pi0   B: phi3, phi0, pi3
@@ -329,7 +338,8 @@ __device__ __forceinline__ bool pair_plane(int i, const PCtx &c, const PairParam
 // TYC > 0: the tile height is a compile-time constant (the default shape),
 // so every staged-plane offset folds into an immediate; TYC = 0: P.ty
 template <int PAIR, int TX, int NP, int TYC>
-__global__ void SB_RKPAIR_BOUNDS(NP) rkpair_kernel(const __grid_constant__ PairParams P) {
+__global__ void __launch_bounds__(lb_threads(TX, NP, TYC), lb_minb(PAIR, TYC))
+    rkpair_kernel(const __grid_constant__ PairParams P) {
     constexpr int TPR = TX / NP;
     constexpr int W = TX + 4;
     extern __shared__ __align__(1024) unsigned char smem[];
