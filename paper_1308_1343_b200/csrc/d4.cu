@@ -66,6 +66,17 @@ __host__ __device__ constexpr int max_threads(int mode, int np) {
 #define SB_D4_ALL10_MINB 1
 #endif
 __host__ __device__ constexpr int min_blocks(int mode) { return all10(mode) ? SB_D4_ALL10_MINB : 1; }
+// Compile-time default shapes (CTA size known exactly): resident CTAs the
+// Laplacian's register allocation must allow (profiles/README.md)
+#ifndef SB_D4_LAP4_MINB_T
+#define SB_D4_LAP4_MINB_T 1
+#endif
+__host__ __device__ constexpr int lb_threads(int mode, int tx, int np, int tyc) {
+    return tyc > 0 ? tx / np * tyc : max_threads(mode, np);
+}
+__host__ __device__ constexpr int lb_minb(int mode, int tyc) {
+    return tyc > 0 && mode == D4_LAP4 ? SB_D4_LAP4_MINB_T : min_blocks(mode);
+}
 
 struct BoxDesc {
     CUtensorMap tmap;          // plane boxes of (TX+4) x (TY+4) x 1 over the source grid
@@ -330,7 +341,8 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
 // TYC > 0: compile-time tile height (the default shapes), so staged-plane
 // offsets fold into immediates; TYC = 0: P.ty
 template <int MODE, int TX, int NP, int TYC>
-__global__ void __launch_bounds__(max_threads(MODE, NP), min_blocks(MODE)) d4_kernel(const __grid_constant__ D4Params P) {
+__global__ void __launch_bounds__(lb_threads(MODE, TX, NP, TYC), lb_minb(MODE, TYC))
+    d4_kernel(const __grid_constant__ D4Params P) {
     constexpr int TPR = TX / NP;    // threads per row
     constexpr int W = TX + 4;       // smem row width (elements)
     extern __shared__ __align__(1024) unsigned char smem[];
