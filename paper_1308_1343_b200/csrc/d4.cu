@@ -444,7 +444,8 @@ template <int MODE, int TX, int NP>
 int launch_mode_tx(const D4Params &P, int nblocks, cudaStream_t st) {
     // the swept default shapes of configs 2 and 4 (32 x 4, point pairs)
     constexpr bool kDefault = TX == 32 && NP == 2 && (MODE == D4_ALL10 || MODE == D4_LAP4);
-    if (kDefault && P.ty == 4) return launch_mode_ty<MODE, TX, NP, 4>(P, nblocks, st);
+    if constexpr (kDefault)
+        if (P.ty == 4) return launch_mode_ty<MODE, TX, NP, 4>(P, nblocks, st);
     return launch_mode_ty<MODE, TX, NP, 0>(P, nblocks, st);
 }
 

@@ -425,7 +425,8 @@ int launch_pair_ty(const PairParams &P, int nblocks, cudaStream_t st) {
 
 template <int PAIR, int TX, int NP>
 int launch_pair_tx(const PairParams &P, int nblocks, cudaStream_t st) {
-    if (TX == 32 && NP == 1 && P.ty == 4) return launch_pair_ty<PAIR, TX, NP, 4>(P, nblocks, st);
+    if constexpr (TX == 32 && NP == 1)
+        if (P.ty == 4) return launch_pair_ty<PAIR, TX, NP, 4>(P, nblocks, st);
     return launch_pair_ty<PAIR, TX, NP, 0>(P, nblocks, st);
 }
 
