@@ -227,6 +227,14 @@ typedef struct sb_zslab {
 SB_API int sb_rk4_stage_zslab(int32_t stage, const sb_rk4_fields *f, sb_space space, sb_rk4_constants c,
                               sb_launch p, const sb_zslab *zs, void *stream);
 
+/* F4 for the pair schedules (sb_rk4_pair): both outputs of a pair launch
+ * write their boundary planes into the neighbouring slabs' ghost planes —
+ * zs[0] names phi_out's neighbours, zs[1] pi_out's (each of the pair's
+ * outputs feeds a stencil of the next launch).  Same conventions as
+ * sb_rk4_stage_zslab; requires SB_LAUNCH_PERIODIC_GHOSTS. */
+SB_API int sb_rk4_pair_zslab(int32_t pair, const sb_rk4_fields *f, sb_space space, sb_rk4_constants c,
+                             sb_launch p, const sb_zslab *zs /* [2] */, void *stream);
+
 /* K6 — config-5 fused right-hand side: 24 inputs (ghost >= 2) -> 24 outputs. */
 SB_API int sb_rhs24(const sb_array *in, const sb_array *out, sb_space space,
              sb_d4_constants k, sb_poly poly, sb_launch p, void *stream);

@@ -28,7 +28,7 @@ EXPORTS = (
     "sb_abi_version", "sb_last_error", "sb_init", "sb_get_device_info", "sb_diff1d",
     "sb_lap7", "sb_d4_all", "sb_d2_all", "sb_lap4_boxes", "sb_ghost_periodic", "sb_rk4_stage",
     "sb_rhs24", "sb_copy_regions", "sb_copy_h2d", "sb_copy_d2h", "sb_copy_h2d_planes", "sb_copy_d2h_planes",
-    "sb_copy_h2d_planes_staged", "sb_rk4_stage_zslab", "sb_rk4_pair",
+    "sb_copy_h2d_planes_staged", "sb_rk4_stage_zslab", "sb_rk4_pair", "sb_rk4_pair_zslab",
 )
 SB_MAX_COPY_JOBS = 64
 
@@ -100,6 +100,8 @@ def _declare(lib) -> None:
         "sb_ghost_periodic": ([sb_array, vp], C.c_int),
         "sb_rk4_stage": ([i32, C.POINTER(sb_rk4_fields), sb_space, sb_rk4_constants, sb_launch, vp], C.c_int),
         "sb_rk4_pair": ([i32, C.POINTER(sb_rk4_fields), sb_space, sb_rk4_constants, sb_launch, vp], C.c_int),
+        "sb_rk4_pair_zslab": ([i32, C.POINTER(sb_rk4_fields), sb_space, sb_rk4_constants, sb_launch,
+                               C.POINTER(sb_zslab), vp], C.c_int),
         "sb_rk4_stage_zslab": ([i32, C.POINTER(sb_rk4_fields), sb_space, sb_rk4_constants, sb_launch,
                                 C.POINTER(sb_zslab), vp], C.c_int),
         "sb_rhs24": ([C.POINTER(sb_array), C.POINTER(sb_array), sb_space, sb_d4_constants, sb_poly, sb_launch, vp],

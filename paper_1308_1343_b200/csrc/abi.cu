@@ -269,6 +269,11 @@ int sb_rk4_stage_zslab(int32_t stage, const sb_rk4_fields *f, sb_space space, sb
 
 int sb_rk4_pair(int32_t pair, const sb_rk4_fields *f, sb_space space, sb_rk4_constants c, sb_launch p,
                 void *stream) {
+    return sb_rk4_pair_zslab(pair, f, space, c, p, nullptr, stream);
+}
+
+int sb_rk4_pair_zslab(int32_t pair, const sb_rk4_fields *f, sb_space space, sb_rk4_constants c, sb_launch p,
+                      const sb_zslab *zs, void *stream) {
     if (!f) return fail(SB_USAGE, "rk4_pair: null fields");
     if (pair < 1 || pair > 4)
         return fail(SB_USAGE, "rk4_pair: pair must be 1/2 (stages 1+2 / 3+4) or 3/4 (Laplacian pairs)");
@@ -325,7 +330,11 @@ int sb_rk4_pair(int32_t pair, const sb_rk4_fields *f, sb_space space, sb_rk4_con
     for (int o = 0; o < no; ++o)
         if ((rc = check_array(out[o], 0, "rk4_pair output")) || (rc = check_space(space, out[o], "rk4_pair")))
             return rc;
-    return launch_rk4_pair(pair - 1, halo, nh, tile, nt, out, no, space, c, p, as_stream(stream));
+    if (zs)
+        for (int a = 0; a < 2; ++a)
+            if (!zs[a].lo_phi_out || !zs[a].hi_phi_out)
+                return fail(SB_USAGE, "rk4_pair_zslab: null neighbour grid");
+    return launch_rk4_pair(pair - 1, halo, nh, tile, nt, out, no, space, c, p, as_stream(stream), zs);
 }
 
 int sb_rhs24(const sb_array *in, const sb_array *out, sb_space space, sb_d4_constants k, sb_poly poly, sb_launch p,

@@ -83,6 +83,8 @@ struct PairParams {
     int ax0, ntx, nty, ty, zc;
     double k2, hdt, dt, dt6;
     int per[3], pghost;        // periodic extents (0: no ghost refresh) and ghost width
+    double *zlo[2], *zhi[2];   // z-image targets of out[0] / out[1] (periodic box: the outputs themselves)
+    int zlo_dz[2], zhi_dz[2];
 };
 
 struct PCtx {
@@ -162,16 +164,19 @@ struct Nbhd {
 
 // store v at off; points within pghost of a periodic face (edge: hoisted
 // per thread in x/y, per plane in z) also write their ghost images
+// (output k = 0 / 1: the x/y images stay in out[k], the z images go to
+// zlo[k] / zhi[k] — out[k] itself for a periodic box, the neighbouring
+// slabs' grids for a z-slab decomposition)
 template <int NP>
-__device__ __forceinline__ void out_periodic(const PairParams &P, double *base, double *at, bool edge, int x,
-                                             int y, int z, const double (&v)[NP], const Lanes<NP> &L) {
+__device__ __forceinline__ void out_periodic(const PairParams &P, int k, double *at, bool edge, int x, int y, int z,
+                                             const double (&v)[NP], const Lanes<NP> &L) {
     store<NP>(at, v, L);
     if (!edge) return;
 #pragma unroll
     for (int j = 0; j < NP; ++j)
         if (L.m[j])
-            store_images(base, P.sy, P.sz, P.per[0], P.per[1], P.per[2], P.pghost, base, P.per[2], base, -P.per[2],
-                         x + j, y, z, v[j]);
+            store_images(P.out[k], P.sy, P.sz, P.per[0], P.per[1], P.per[2], P.pghost, P.zlo[k], P.zlo_dz[k],
+                         P.zhi[k], P.zhi_dz[k], x + j, y, z, v[j]);
 }
 
 template <int PAIR, int TX, int NP, int R>
@@ -290,13 +295,13 @@ __device__ __forceinline__ bool pair_plane(int i, const PCtx &c, const PairParam
             af[j] = add(pi0, mul(2.0, pi2));
             ap[j] = add(la[j], mul(2.0, lb[j]));
         }
-        out_periodic<NP>(P, P.out[0], rg.o[0], edge, x, y, zc, f3, L);
-        out_periodic<NP>(P, P.out[1], rg.o[1], edge, x, y, zc, p3, L);
+        out_periodic<NP>(P, 0, rg.o[0], edge, x, y, zc, f3, L);
+        out_periodic<NP>(P, 1, rg.o[1], edge, x, y, zc, p3, L);
         store<NP>(rg.o[2], af, L);
         store<NP>(rg.o[3], ap, L);
     } else if constexpr (PAIR == PAIR_LA) {
-        out_periodic<NP>(P, P.out[0], rg.o[0], edge, x, y, zc, la, L);   // L1 = Lap(phi0)
-        out_periodic<NP>(P, P.out[1], rg.o[1], edge, x, y, zc, lb, L);   // L2 = Lap(phi2)
+        out_periodic<NP>(P, 0, rg.o[0], edge, x, y, zc, la, L);   // L1 = Lap(phi0)
+        out_periodic<NP>(P, 1, rg.o[1], edge, x, y, zc, lb, L);   // L2 = Lap(phi2)
     } else if constexpr (PAIR == PAIR_LB) {
         // la = L3, lb = L4; the stage 1-3 quantities are re-formed from phi0, pi0, L1, L2
         double fn[NP], pn[NP];
@@ -311,8 +316,8 @@ __device__ __forceinline__ bool pair_plane(int i, const PCtx &c, const PairParam
             fn[j] = add(phi0, mul(P.dt6, add(acf, pi4)));
             pn[j] = add(pi0, mul(P.dt6, add(acp, lb[j])));
         }
-        out_periodic<NP>(P, P.out[0], rg.o[0], edge, x, y, zc, fn, L);
-        out_periodic<NP>(P, P.out[1], rg.o[1], edge, x, y, zc, pn, L);
+        out_periodic<NP>(P, 0, rg.o[0], edge, x, y, zc, fn, L);
+        out_periodic<NP>(P, 1, rg.o[1], edge, x, y, zc, pn, L);
     } else {
         // stage 3: pi4 = pi0 + dt L3, acc_phi += 2 pi3, acc_pi += 2 L3   (phi4 = phi0 + dt pi3)
         // stage 4: phi' = phi0 + (dt/6)(acc_phi + pi4), pi' = pi0 + (dt/6)(acc_pi + L4)
@@ -327,8 +332,8 @@ __device__ __forceinline__ bool pair_plane(int i, const PCtx &c, const PairParam
             fn[j] = add(phi0, mul(P.dt6, add(acf3, pi4)));
             pn[j] = add(pi0, mul(P.dt6, add(acp3, lb[j])));
         }
-        out_periodic<NP>(P, P.out[0], rg.o[0], edge, x, y, zc, fn, L);
-        out_periodic<NP>(P, P.out[1], rg.o[1], edge, x, y, zc, pn, L);
+        out_periodic<NP>(P, 0, rg.o[0], edge, x, y, zc, fn, L);
+        out_periodic<NP>(P, 1, rg.o[1], edge, x, y, zc, pn, L);
     }
 #pragma unroll
     for (int k = 0; k < n_out(PAIR); ++k) rg.o[k] += P.sz;
@@ -443,7 +448,8 @@ int launch_pair_np(const PairParams &P, int tx, int nblocks, cudaStream_t st) {
 }  // namespace
 
 int launch_rk4_pair(int pair, const sb_array *halo, int nh, const sb_array *tile, int nt, const sb_array *out, int no,
-                    const sb_space &sp, const sb_rk4_constants &k, const sb_launch &p, cudaStream_t st) {
+                    const sb_space &sp, const sb_rk4_constants &k, const sb_launch &p, cudaStream_t st,
+                    const sb_zslab *zs) {
     const int TX = p.tile_x, TY = p.tile_y, ZC = p.z_chunk;
     const int NP = (p.flags & SB_LAUNCH_SCALAR) ? 1 : 2;
     if (TX != 32 && TX != 64 && TX != 128) return fail(SB_USAGE, "tile_x must be 32, 64 or 128");
@@ -505,6 +511,20 @@ int launch_rk4_pair(int pair, const sb_array *halo, int nh, const sb_array *tile
         P.per[1] = O.ny;
         P.per[2] = O.nz;
         P.pghost = O.ghost;
+        for (int a = 0; a < 2; ++a) {
+            if (zs) {   // z-slab decomposition: z images go to the neighbouring slabs
+                P.zlo[a] = zs[a].lo_phi_out;
+                P.zlo_dz[a] = zs[a].lo_dz;
+                P.zhi[a] = zs[a].hi_phi_out;
+                P.zhi_dz[a] = zs[a].hi_dz;
+            } else {
+                P.zlo[a] = P.zhi[a] = out[a].origin;
+                P.zlo_dz[a] = O.nz;
+                P.zhi_dz[a] = -O.nz;
+            }
+        }
+    } else if (zs) {
+        return fail(SB_USAGE, "z-slab halo stores need SB_LAUNCH_PERIODIC_GHOSTS");
     }
     const long long nb = (long long)P.ntx * P.nty * ntz;
     if (nb > 0x7fffffffLL) return fail(SB_RESOURCE, "too many tiles for one launch");

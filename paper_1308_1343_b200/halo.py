@@ -10,6 +10,12 @@ straight into the neighbour's phi ghost planes as part of its stores
 on the same GPU.  The only synchronisation left is "every slab finished
 stage s" before stage s+1 reads its ghosts — a barrier, no data movement.
 
+The stage pairs (``sb_rk4_pair_zslab``) work the same way with two launches
+and two barriers per step instead of four: both outputs of a pair launch
+(L1, L2 — or phi3, pi3 — and then phi', pi') write their boundary planes
+into the neighbours' ghost planes, since each feeds a stencil of the next
+launch.
+
 * :class:`WaveRK4Slabs` — R slabs in one process (one GPU): the fused
   exchange exercised end to end without extra GPUs.
 * :class:`ZSlabRank` — one slab per process/rank; neighbour buffers are
@@ -30,6 +36,16 @@ BUFFERS = ("phi0", "pi0", "phi_a", "pi_a", "phi_b", "pi_b", "acc_phi", "acc_pi")
 # (stage, phi_s, pi_s, phi_out, pi_out) of one classical RK4 step
 STAGES = ((1, "phi0", "pi0", "phi_a", "pi_a"), (2, "phi_a", "pi_a", "phi_b", "pi_b"),
           (3, "phi_b", "pi_b", "phi_a", "pi_a"), (4, "phi_a", "pi_a", "phi_b", "pi_b"))
+# (pair, phi_s, pi_s, phi_out, pi_out) of the pair schedules (kernels.WaveRK4)
+PAIRS = {"lap_pairs": ((3, "phi0", "pi0", "phi_a", "pi_a"), (4, "phi_a", "pi_a", "phi_b", "pi_b")),
+         "pairs": ((1, "phi0", "pi0", "phi_a", "pi_a"), (2, "phi_a", "pi_a", "phi_b", "pi_b"))}
+SCHEDULES = ("stages", "lap_pairs", "pairs")
+
+
+def _launches(schedule: str):
+    if schedule not in SCHEDULES:
+        raise UsageError(f"unknown z-slab RK4 schedule {schedule!r}")
+    return STAGES if schedule == "stages" else PAIRS[schedule]
 
 
 def z_cuts(n: int, parts: int, ghost: int) -> list[int]:
@@ -72,15 +88,32 @@ def launch_stage(s: Slab, stage: tuple, c: WaveConstants, params: LaunchParams, 
               _lib.launch_of(params, _lib.SB_LAUNCH_PERIODIC_GHOSTS), C.byref(zs), stream_ptr(stream))
 
 
+def launch_pair(s: Slab, pair: tuple, c: WaveConstants, params: LaunchParams, lo: tuple, lo_dz: int, hi: tuple,
+                hi_dz: int, stream=None) -> None:
+    """One pair launch of slab s; lo / hi = (phi_out, pi_out) origins of the
+    lower / upper neighbours."""
+    k, phi_s, pi_s, phi_out, pi_out = pair
+    f = _fields(s, phi_s, pi_s, phi_out, pi_out)
+    zs = (_lib.sb_zslab * 2)(_lib.sb_zslab(lo[0], lo_dz, hi[0], hi_dz), _lib.sb_zslab(lo[1], lo_dz, hi[1], hi_dz))
+    _lib.call("sb_rk4_pair_zslab", k, C.byref(f), _lib.space((0, 0, 0), (s.n, s.n, s.nz)), _consts(c),
+              _lib.launch_of(params, _lib.SB_LAUNCH_PERIODIC_GHOSTS), zs, stream_ptr(stream))
+
+
+def _default_params(schedule: str) -> LaunchParams:
+    return LaunchParams(64, 4, 16, 1) if schedule == "stages" else LaunchParams(32, 4, 64, 1)
+
+
 class WaveRK4Slabs:
     """R z-slabs of one periodic n^3 box in one process.  Each stage launch of
     slab r writes its boundary planes into slabs r-1 / r+1 (ring)."""
 
-    def __init__(self, n: int, parts: int, ghost: int, c: WaveConstants, device=None):
+    def __init__(self, n: int, parts: int, ghost: int, c: WaveConstants, device=None, schedule: str = "stages"):
         self.n, self.g, self.c = n, ghost, c
+        self.schedule = schedule
+        self.launches = _launches(schedule)
         cuts = z_cuts(n, parts, ghost)
         self.slabs = [Slab(n, cuts[j], cuts[j + 1] - cuts[j], ghost, device) for j in range(parts)]
-        self.params = LaunchParams(64, 4, 16, 1)
+        self.params = _default_params(schedule)
 
     def upload(self, phi_global, pi_global) -> None:
         for s in self.slabs:
@@ -89,12 +122,16 @@ class WaveRK4Slabs:
     def step(self, params: LaunchParams | None = None, stream=None) -> None:
         p = params or self.params
         R = len(self.slabs)
-        for stage in STAGES:
-            out = stage[3]
+        for stage in self.launches:
+            out, out2 = stage[3], stage[4]
             for r, s in enumerate(self.slabs):
                 lo, hi = self.slabs[(r - 1) % R], self.slabs[(r + 1) % R]
-                launch_stage(s, stage, self.c, p, getattr(lo, out).origin_ptr, lo.nz,
-                             getattr(hi, out).origin_ptr, -s.nz, stream)
+                if self.schedule == "stages":
+                    launch_stage(s, stage, self.c, p, getattr(lo, out).origin_ptr, lo.nz,
+                                 getattr(hi, out).origin_ptr, -s.nz, stream)
+                else:
+                    launch_pair(s, stage, self.c, p, (getattr(lo, out).origin_ptr, getattr(lo, out2).origin_ptr),
+                                lo.nz, (getattr(hi, out).origin_ptr, getattr(hi, out2).origin_ptr), -s.nz, stream)
 
     def result(self, name: str = "phi_b", with_ghosts: bool = False):
         import numpy as np
@@ -111,15 +148,19 @@ class ZSlabRank:
     multi-GPU node); ``dist`` is an initialised ``torch.distributed``
     module/group for the handle exchange and ``barrier()`` orders stages."""
 
-    def __init__(self, n: int, rank: int, world: int, ghost: int, c: WaveConstants, dist, device=None):
+    def __init__(self, n: int, rank: int, world: int, ghost: int, c: WaveConstants, dist, device=None,
+                 schedule: str = "stages"):
         import torch
         self.n, self.g, self.c = n, ghost, c
         self.rank, self.world, self.dist = rank, world, dist
+        self.schedule = schedule
+        self.launches = _launches(schedule)
         cuts = z_cuts(n, world, ghost)
         self.slab = Slab(n, cuts[rank], cuts[rank + 1] - cuts[rank], ghost, device)
-        self.params = LaunchParams(64, 4, 16, 1)
+        self.params = _default_params(schedule)
+        shared = ("phi_a", "phi_b") if schedule == "stages" else ("phi_a", "pi_a", "phi_b", "pi_b")
         mine = {name: (getattr(self.slab, name).storage.untyped_storage()._share_cuda_(),
-                       getattr(self.slab, name).offset) for name in ("phi_a", "phi_b")}
+                       getattr(self.slab, name).offset) for name in shared}
         everyone = [None] * world
         dist.all_gather_object(everyone, (self.slab.nz, mine))
         self._keep = []
@@ -145,8 +186,12 @@ class ZSlabRank:
     def step(self, params: LaunchParams | None = None) -> None:
         p = params or self.params
         lo, hi = (self.rank - 1) % self.world, (self.rank + 1) % self.world
-        for stage in STAGES:
-            out = stage[3]
-            launch_stage(self.slab, stage, self.c, p, self.peer[(lo, out)], self.peer_nz[lo],
-                         self.peer[(hi, out)], -self.slab.nz)
+        for stage in self.launches:
+            out, out2 = stage[3], stage[4]
+            if self.schedule == "stages":
+                launch_stage(self.slab, stage, self.c, p, self.peer[(lo, out)], self.peer_nz[lo],
+                             self.peer[(hi, out)], -self.slab.nz)
+            else:
+                launch_pair(self.slab, stage, self.c, p, (self.peer[(lo, out)], self.peer[(lo, out2)]),
+                            self.peer_nz[lo], (self.peer[(hi, out)], self.peer[(hi, out2)]), -self.slab.nz)
             self.barrier()
