@@ -165,6 +165,15 @@ SB_API int sb_diff1d(int32_t kind, double *dst, const double *src, int32_t n, vo
 SB_API int sb_lap7(sb_array dst, sb_array src, sb_space space, double c0, double c1,
             sb_launch p, void *stream);
 
+/* K1 iterated — `iters` Jacobi sweeps of the same update in ONE persistent
+ * cooperative launch (the reference's run_serial loop, stencil.py:55-65):
+ * sweep k reads a and writes b for even k, the reverse for odd k, with a
+ * grid-wide barrier between sweeps; the result is in b for odd `iters`, in
+ * a for even.  Both grids need ghost >= 1 with the same (fixed) boundary
+ * values.  Bit-identical to `iters` sb_lap7 calls. */
+SB_API int sb_lap7_iterate(sb_array a, sb_array b, sb_space space, double c0, double c1, int32_t iters,
+                           sb_launch p, void *stream);
+
 /* K2 — all ten 4th-order outputs of one box (config 2).  out[i] follows
  * SB_N_D4_OUT order.  src ghost >= 2. */
 SB_API int sb_d4_all(const sb_array *out, sb_array src, sb_space space,

@@ -28,7 +28,7 @@ EXPORTS = (
     "sb_abi_version", "sb_last_error", "sb_init", "sb_get_device_info", "sb_diff1d",
     "sb_lap7", "sb_d4_all", "sb_d2_all", "sb_lap4_boxes", "sb_ghost_periodic", "sb_rk4_stage",
     "sb_rhs24", "sb_copy_regions", "sb_copy_h2d", "sb_copy_d2h", "sb_copy_h2d_planes", "sb_copy_d2h_planes",
-    "sb_copy_h2d_planes_staged", "sb_rk4_stage_zslab", "sb_rk4_pair", "sb_rk4_pair_zslab",
+    "sb_copy_h2d_planes_staged", "sb_rk4_stage_zslab", "sb_rk4_pair", "sb_rk4_pair_zslab", "sb_lap7_iterate",
 )
 SB_MAX_COPY_JOBS = 64
 
@@ -94,6 +94,7 @@ def _declare(lib) -> None:
         "sb_get_device_info": ([C.POINTER(sb_device_info)], C.c_int),
         "sb_diff1d": ([i32, vp, vp, i32, vp], C.c_int),
         "sb_lap7": ([sb_array, sb_array, sb_space, C.c_double, C.c_double, sb_launch, vp], C.c_int),
+        "sb_lap7_iterate": ([sb_array, sb_array, sb_space, C.c_double, C.c_double, i32, sb_launch, vp], C.c_int),
         "sb_d4_all": ([C.POINTER(sb_array), sb_array, sb_space, sb_d4_constants, sb_launch, vp], C.c_int),
         "sb_d2_all": ([C.POINTER(sb_array), sb_array, sb_space, sb_d4_constants, sb_launch, vp], C.c_int),
         "sb_lap4_boxes": ([C.POINTER(sb_box_job), i32, sb_d4_constants, sb_launch, vp], C.c_int),

@@ -5,8 +5,9 @@ run the 7-point Jacobi demo serially, with the naive static split and
 tuned, check the outputs are bit-identical, write the per-iteration CSV
 ``impl,iter,elapsed_ns,phase,is_best`` and print the summary; exit 0 when
 bit-identical, 1 otherwise, 2 on usage/resource errors (cli.py:288-295).
-The device adds a fourth implementation, ``graphed`` (the same sweeps
-captured in a CUDA graph).  ``config-bench`` times one BASELINE.json
+The device adds two implementations: ``graphed`` (the same sweeps captured
+in a CUDA graph) and ``persistent`` (all sweeps in one cooperative launch
+with a grid barrier between them).  ``config-bench`` times one BASELINE.json
 configuration (1..5) with the run-time tuner.  ``tune-sim`` runs the
 tuner against a synthetic cost surface (reference cli.py:212-226; no GPU).
 
@@ -52,7 +53,9 @@ def cmd_stencil_bench(args) -> int:
     naive = stencil.run_naive(n, iters, args.seed, topo.n_coarse_threads)
     tuned, tuner = stencil.run_tuned(n, iters, args.seed, topo)
     graphed = stencil.run_graphed(n, iters - iters % 2, args.seed) if iters >= 2 else None
+    persistent = stencil.run_persistent(n, iters, args.seed)
     ok = stencil.bit_identical(serial.final, naive.final) and stencil.bit_identical(serial.final, tuned.final)
+    ok = ok and stencil.bit_identical(serial.final, persistent.final)
     if graphed is not None and iters % 2 == 0:
         ok = ok and stencil.bit_identical(serial.final, graphed.final)
     rows = ["impl,iter,elapsed_ns,phase,is_best"]
@@ -62,6 +65,7 @@ def cmd_stencil_bench(args) -> int:
              for i, (t, r) in enumerate(zip(tuned.iter_seconds, tuner.log))]
     if graphed is not None:
         rows += [f"graphed,{i},{int(t * 1e9)},," for i, t in enumerate(graphed.iter_seconds)]
+    rows += [f"persistent,{i},{int(t * 1e9)},," for i, t in enumerate(persistent.iter_seconds)]
     if args.out:
         Path(args.out).write_text("\n".join(rows) + "\n")
     tail = max(1, min(20, iters // 2))
@@ -70,6 +74,8 @@ def cmd_stencil_bench(args) -> int:
             f"tuned(last {tail}) {_med(tuned.iter_seconds[-tail:]):.6f}")
     if graphed is not None:
         line += f"  graphed {_med(graphed.iter_seconds):.6f}"
+    if persistent.iter_seconds:
+        line += f"  persistent {_med(persistent.iter_seconds):.6f}"
     print(line)
     return 0 if ok else 1
 

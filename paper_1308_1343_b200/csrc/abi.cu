@@ -162,6 +162,15 @@ int sb_lap7(sb_array dst, sb_array src, sb_space space, double c0, double c1, sb
     return launch_lap7(dst, src, space, c0, c1, p, as_stream(stream));
 }
 
+int sb_lap7_iterate(sb_array a, sb_array b, sb_space space, double c0, double c1, int32_t iters, sb_launch p,
+                    void *stream) {
+    int rc;
+    if ((rc = check_array(a, 1, "lap7_iterate a")) || (rc = check_array(b, 1, "lap7_iterate b"))) return rc;
+    if ((rc = check_space(space, a, "lap7_iterate")) || (rc = check_space(space, b, "lap7_iterate b"))) return rc;
+    if (a.origin == b.origin) return fail(SB_USAGE, "lap7_iterate: a and b must be different grids");
+    return launch_lap7_iterate(a, b, space, c0, c1, iters, p, as_stream(stream));
+}
+
 namespace {
 int all10(int mode, const char *nm, const sb_array *out, sb_array src, sb_space space, sb_d4_constants k,
           sb_launch p, void *stream) {

@@ -22,6 +22,8 @@ int make_tmap(CUtensorMap *m, const sb_array &a, int bx, int by, int bz);
 // Launchers (one per kernel family, defined next to their kernels).
 int launch_lap7(const sb_array &dst, const sb_array &src, const sb_space &sp, double c0, double c1,
                 const sb_launch &p, cudaStream_t st);
+int launch_lap7_iterate(const sb_array &a, const sb_array &b, const sb_space &sp, double c0, double c1, int iters,
+                        const sb_launch &p, cudaStream_t st);
 int launch_diff1d(int kind, double *dst, const double *src, int n, cudaStream_t st);
 
 // RK stages: RK1 = stage 1, RK2 = stage 2 (acc_phi = pi0 + 2 pi_s: stage 1 never

@@ -90,6 +90,16 @@ class Laplacian7(DeviceKernel):
         _lib.call("sb_lap7", self.dst.abi(), self.src.abi(), _local(space, self.src), self.c0, self.c1,
                   _lib.launch_of(params, self.extra_flags), stream_ptr(stream))
 
+    def iterate(self, a: DeviceGrid, b: DeviceGrid, space: IndexSpace, iters: int,
+                params: LaunchParams | None = None, stream=None) -> DeviceGrid:
+        """``iters`` Jacobi sweeps a -> b -> a ... in one persistent launch
+        (``sb_lap7_iterate``); returns the grid holding the result."""
+        if a.extents != b.extents or a.lower != b.lower:
+            raise UsageError("a and b must cover the same box")
+        _lib.call("sb_lap7_iterate", a.abi(), b.abi(), _local(space, a), self.c0, self.c1, int(iters),
+                  _lib.launch_of(params or self.default_params, self.extra_flags), stream_ptr(stream))
+        return b if iters % 2 else a
+
 
 class FourthOrderAll(DeviceKernel):
     """K2 — all ten 4th-order outputs of a box (config 2): Dx Dy Dz Dxx Dyy Dzz Dxy Dxz Dyz Lap4."""

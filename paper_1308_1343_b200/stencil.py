@@ -126,6 +126,21 @@ def run_graphed(n: int, iters: int, seed: int, c0: float = C0, c1: float = C1, b
     return out
 
 
+def run_persistent(n: int, iters: int, seed: int, c0: float = C0, c1: float = C1) -> StencilRun:
+    """``run_serial`` as ONE persistent cooperative launch
+    (``sb_lap7_iterate``): the CTAs stay resident and meet at a grid barrier
+    between sweeps; iter_seconds are the per-sweep average of the launch."""
+    a, b = _buffers(n, seed)
+    out = StencilRun(np.empty(0))
+    if iters > 0:
+        k = Laplacian7(b, a, c0, c1)
+        with _Timer(True) as tm:
+            k.iterate(a, b, _space(n), iters)
+        out.iter_seconds = [tm.elapsed() / iters] * iters
+    out.final = (b if iters % 2 else a).download(with_ghosts=True)
+    return out
+
+
 def bit_identical(a: np.ndarray, b: np.ndarray) -> bool:
     """stencil.py:97-98."""
     return a.shape == b.shape and a.tobytes() == b.tobytes()

@@ -79,6 +79,21 @@ def test_reference_demo_drivers_bit_identical(golden):
     assert len(tuner.log) == d["n64_iters"]
 
 
+@pytest.mark.parametrize("n,iters", [(64, 100), (16, 8), (19, 7), (64, 1), (130, 6)])
+def test_persistent_sweeps_match_serial(golden, n, iters):
+    """All sweeps in one cooperative launch (grid barrier between sweeps)
+    give the serial driver's bits, odd and even counts, ragged extents."""
+    from paper_1308_1343_b200 import stencil
+    meta, a = golden
+    d = meta["demo"]
+    got = stencil.run_persistent(n, iters, d["seed"]).final
+    if (n, iters) == (64, d["n64_iters"]):
+        assert inputs.sha256(got) == d["n64_final_sha256"]
+    if (n, iters) == (16, d["n16_iters"]):
+        assert bits_equal(got, a["demo16_final"])
+    assert stencil.bit_identical(got, stencil.run_serial(n, iters, d["seed"]).final)
+
+
 def test_graphed_demo_matches_reference(golden):
     """The CUDA-graph-captured sweep loop gives the reference's bits."""
     from paper_1308_1343_b200 import stencil
