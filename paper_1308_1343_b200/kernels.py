@@ -73,8 +73,8 @@ class Laplacian7(DeviceKernel):
 
     site_id = "laplacian3d"
     space_kind = LAP7_SPACE
-    # best of the CUDA-graph sweep at 64^3 (profiles/r01/v2_sweep_c1_graph.jsonl)
-    default_params = LaunchParams(64, 8, 4)
+    # best of the CUDA-graph sweep at 64^3 (profiles/r01/v12_sweep_c1_graph.log)
+    default_params = LaunchParams(64, 8, 2)
 
     def __init__(self, dst: DeviceGrid, src: DeviceGrid, c0: float, c1: float):
         if src.ghost < 1:
