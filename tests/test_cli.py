@@ -27,7 +27,7 @@ def test_stencil_bench_bit_identical_and_csv(tmp_path, capsys):
     assert lines[0] == "impl,iter,elapsed_ns,phase,is_best"
     assert all(len(l.split(",")) == 5 for l in lines)
     impls = {l.split(",")[0] for l in lines[1:]}
-    assert impls == {"serial", "naive", "tuned", "graphed"}
+    assert impls == {"serial", "naive", "tuned", "graphed", "persistent"}
     phases = {l.split(",")[3] for l in lines[1:] if l.startswith("tuned")}
     assert phases <= {"warmup", "initial", "climbing", "excursion"}
 
