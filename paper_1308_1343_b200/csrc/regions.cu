@@ -4,8 +4,10 @@
 // zone) is host-side region algebra — expand, intersect (the reference's
 // bboxset operations, bboxset.py:339-385, lattice.py:156-191) — computed in
 // level.ghost_schedule.  The device side is one launch over all copies of a
-// schedule chunk: blockIdx -> (job, block of points) through a prefix table,
-// one thread per point, x fastest so rows are coalesced.
+// schedule chunk: a CTA takes whole rows (blockIdx -> (job, row) through a
+// prefix table over rows, one 32-bit divide per row), its threads walk the
+// row in x, so accesses are coalesced and no per-point index arithmetic is
+// paid.
 #include <cstring>
 
 #include "common.cuh"
@@ -18,27 +20,25 @@ namespace {
 struct CopyDesc {
     Grid dst, src;
     int dlo[3], slo[3], ext[3];
-    long long begin;     // first linear point index of this job
+    int row_begin;       // first row (y, z pair) of this job in the launch
 };
 
 struct CopyParams {
     CopyDesc job[SB_MAX_COPY_JOBS];
     int njobs;
-    long long total;
+    int rows;
 };
 
-__global__ void copy_regions_kernel(const __grid_constant__ CopyParams P) {
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < P.total;
-         t += (long long)gridDim.x * blockDim.x) {
-        int j = 0;
-        while (j + 1 < P.njobs && t >= P.job[j + 1].begin) ++j;
+__global__ void __launch_bounds__(128) copy_regions_kernel(const __grid_constant__ CopyParams P) {
+    int j = 0;
+    for (int row = blockIdx.x; row < P.rows; row += gridDim.x) {
+        while (j + 1 < P.njobs && row >= P.job[j + 1].row_begin) ++j;   // rows ascend per CTA
         const CopyDesc &J = P.job[j];
-        long long r = t - J.begin;
-        const int x = (int)(r % J.ext[0]);
-        r /= J.ext[0];
-        const int y = (int)(r % J.ext[1]);
-        const int z = (int)(r / J.ext[1]);
-        *J.dst.at(J.dlo[0] + x, J.dlo[1] + y, J.dlo[2] + z) = *J.src.at(J.slo[0] + x, J.slo[1] + y, J.slo[2] + z);
+        const int r = row - J.row_begin;
+        const int y = r % J.ext[1], z = r / J.ext[1];
+        double *d = J.dst.at(J.dlo[0], J.dlo[1] + y, J.dlo[2] + z);
+        const double *s = J.src.at(J.slo[0], J.slo[1] + y, J.slo[2] + z);
+        for (int x = threadIdx.x; x < J.ext[0]; x += blockDim.x) d[x] = s[x];
     }
 }
 
@@ -78,7 +78,7 @@ int launch_copy_regions(const sb_copy_job *jobs, int njobs, cudaStream_t st) {
     if (njobs < 0 || njobs > SB_MAX_COPY_JOBS) return fail(SB_RESOURCE, "copy_regions: 0..SB_MAX_COPY_JOBS jobs per call");
     CopyParams P;
     memset(&P, 0, sizeof(P));
-    long long total = 0;
+    long long rows = 0;
     int n = 0;
     for (int j = 0; j < njobs; ++j) {
         const sb_copy_job &J = jobs[j];
@@ -93,16 +93,15 @@ int launch_copy_regions(const sb_copy_job *jobs, int njobs, cudaStream_t st) {
             D.slo[d] = J.src_lo[d];
             D.ext[d] = J.ext[d];
         }
-        D.begin = total;
-        total += (long long)J.ext[0] * J.ext[1] * J.ext[2];
+        D.row_begin = (int)rows;
+        rows += (long long)J.ext[1] * J.ext[2];
+        if (rows > 0x7fffffffLL) return fail(SB_RESOURCE, "copy_regions: too many rows for one launch");
     }
-    if (total == 0) return SB_OK;
+    if (rows == 0) return SB_OK;
     P.njobs = n;
-    P.total = total;
-    const int threads = 256;
-    long long blocks = (total + threads - 1) / threads;
-    if (blocks > 148LL * 32) blocks = 148LL * 32;
-    copy_regions_kernel<<<(unsigned)blocks, threads, 0, st>>>(P);
+    P.rows = (int)rows;
+    const long long blocks = rows < 148LL * 16 ? rows : 148LL * 16;
+    copy_regions_kernel<<<(unsigned)blocks, 128, 0, st>>>(P);
     return check_cuda(cudaGetLastError(), "copy_regions_kernel launch");
 }
 
