@@ -124,3 +124,33 @@ def test_topology_from_device():
     from paper_1308_1343_b200.tuner import TopologyConfig
     t = TopologyConfig().with_device()
     assert t.sm_count >= 100 and t.smem_per_block >= 200 * 1024 and t.l2_bytes > 50 * 2 ** 20
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_levels_random_launches(seed):
+    """Random bboxset-style levels (a random box minus a random box, plus an
+    unrelated box at a negative offset), random launch shapes: every box of
+    the level matches the oracle."""
+    import random
+
+    from paper_1308_1343_b200.configs import C4Level
+    from paper_1308_1343_b200.level import Box, box_difference
+    rng = random.Random(seed)
+    lo = tuple(rng.randint(-20, 20) for _ in range(3))
+    ext = tuple(rng.randint(6, 40) for _ in range(3))
+    outer = Box(lo, tuple(a + e - 1 for a, e in zip(lo, ext)))
+    hlo = tuple(a + rng.randint(1, e - 2) for a, e in zip(lo, ext))
+    hole = Box(hlo, tuple(min(a + e - 1, h + rng.randint(0, 10)) for a, e, h in zip(lo, ext, hlo)))
+    boxes = box_difference(outer, hole)
+    far = tuple(rng.randint(-200, -100) for _ in range(3))
+    boxes.append(Box(far, tuple(f + rng.randint(1, 20) for f in far)))
+    p = C4Level(n=64, seed=seed, boxes=boxes).setup()
+    tx = rng.choice([32, 64, 128])
+    pp = rng.choice([1, 2])
+    ty = rng.choice([t for t in (1, 2, 4, 8) if (tx // pp) * t % 32 == 0 and (tx // pp) * t <= 512])
+    p.run(LaunchParams(tx, ty, rng.randint(1, 40), pp))
+    for b, u, got in zip(p.boxes, p.host_u, p.outputs()):
+        nx, ny, nz = b.extents
+        want = np.empty((nz, ny, nx))
+        oracle.lap4(want, u, 2, (0, nx, 0, ny, 0, nz), p.k.k2)
+        assert same(got, want), (b, tx, ty, pp)
