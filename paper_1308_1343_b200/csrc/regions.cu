@@ -49,15 +49,16 @@ bool inside(const sb_array &a, const int lo[3], const int ext[3], int halo) {
     return true;
 }
 
-// Dense rows (w doubles each, rows_y rows per plane) -> padded rows of a grid.
-__global__ void unpack_rows_kernel(double *dst, long long sy, long long sz, int w, int rows_y, const double *src,
-                                   long long n) {
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
-        const long long row = t / w;
-        const int col = (int)(t - row * w);
+// Dense rows (w doubles each, rows_y rows per plane) -> padded rows of a
+// grid: a CTA per row (grid-stride over rows), threads along the row.
+__global__ void __launch_bounds__(256) unpack_rows_kernel(double *dst, long long sy, long long sz, int w, int rows_y,
+                                                          const double *src, long long rows) {
+    for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
         const int y = (int)(row % rows_y);
         const long long z = row / rows_y;
-        dst[col + y * sy + z * sz] = src[t];
+        double *d = dst + y * sy + z * sz;
+        const double *s = src + row * w;
+        for (int c = threadIdx.x; c < w; c += blockDim.x) d[c] = s[c];
     }
 }
 
@@ -65,11 +66,10 @@ __global__ void unpack_rows_kernel(double *dst, long long sy, long long sz, int 
 
 int launch_unpack_rows(double *dst, long long sy, long long sz, int w, int rows_y, const double *src, long long n,
                        cudaStream_t st) {
-    if (n <= 0) return SB_OK;
-    const int threads = 256;
-    long long blocks = (n + threads - 1) / threads;
-    if (blocks > 148LL * 32) blocks = 148LL * 32;
-    unpack_rows_kernel<<<(unsigned)blocks, threads, 0, st>>>(dst, sy, sz, w, rows_y, src, n);
+    if (n <= 0 || w <= 0) return SB_OK;
+    const long long rows = n / w;
+    const long long blocks = rows < 148LL * 16 ? rows : 148LL * 16;
+    unpack_rows_kernel<<<(unsigned)blocks, 256, 0, st>>>(dst, sy, sz, w, rows_y, src, rows);
     return check_cuda(cudaGetLastError(), "unpack_rows_kernel launch");
 }
 
