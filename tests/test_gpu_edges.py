@@ -71,9 +71,12 @@ def test_offset_box_level_coordinates():
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 30])
 def test_rk4_small_and_ragged_periodic(n, schedule):
     from paper_1308_1343_b200.configs import C3WaveRK4
+    from paper_1308_1343_b200.errors import UsageError
     g = 2
-    if n < g:
-        pytest.skip("periodic ghost width must not exceed the extent")
+    if n < g:   # a periodic ghost shell wider than the box is rejected, not mis-filled
+        with pytest.raises(UsageError):
+            C3WaveRK4(n=n, seed=n, schedule=schedule).setup().run(LaunchParams(32, 4, 5, 1))
+        return
     p = C3WaveRK4(n=n, seed=n, schedule=schedule).setup()
     p.run(LaunchParams(32, 4, 5, 1))
     wphi, wpi = oracle.rk4_step(p.host_phi, p.host_pi, g, p.c)
