@@ -33,7 +33,7 @@ def test_stencil_bench_bit_identical_and_csv(tmp_path, capsys):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("config", [1, 4])
+@pytest.mark.parametrize("config", [1, 2, 3, 4, 5])
 def test_config_bench_runs(config, capsys):
     import json
     assert main(["config-bench", "--config", str(config), "--iters", "3", "--tune", "6"]) == 0
