@@ -98,3 +98,34 @@ def test_gloo_world2_level_sweep_matches_single_process():
                 if jj == j:
                     got[z0:z1] = arr
         assert got.tobytes() == want.tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("impl", ["ours", "reference"])
+def test_bench_under_torchrun_two_ranks(impl):
+    """bench.py launched the way the driver launches N>1 (torchrun, one
+    process per rank), both ranks on the one GPU here with the gloo backend
+    (plumbing only: the ranks never wait on each other's kernels): rank 0
+    prints exactly one JSON line with the whole-job value."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    port = 29400 + os.getpid() % 300 + (0 if impl == "ours" else 300)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(root / "bench.py"), "--gpus", "2",
+           "--steps", "3", "--warmup", "3", "--impl", impl]
+    if impl == "ours":
+        cmd += ["--tune", "0", "--no-cpu", "--e2e-steps", "3", "--sustained-steps", "0"]
+    env = dict(os.environ, STENCIL_BENCH_BACKEND="gloo")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    rec = json.loads(lines[0])
+    assert rec["value"] > 0 and rec["n_gpus"] == 2
+    if impl == "ours":
+        assert rec["scaling"] == "weak" and rec["gpu_launches"] == 3
+    else:
+        assert rec["impl"] == "reference"
