@@ -48,3 +48,16 @@ def test_tune_sim(tmp_path, capsys):
     assert "seeds within 10%" in capsys.readouterr().out
     rows = out.read_text().splitlines()
     assert rows[0] == "seed,best_cost,evals_to_within_10pct,total_cost" and len(rows) == 21
+
+
+@pytest.mark.gpu
+def test_quickstart_example_runs():
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    r = subprocess.run([sys.executable, str(root / "examples" / "quickstart.py")], capture_output=True, text=True,
+                       timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = r.stdout
+    assert "jacobi:" in out and "level: 3 boxes" in out and "wave:" in out and "derivatives: 10 outputs" in out
