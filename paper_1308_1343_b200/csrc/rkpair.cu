@@ -47,6 +47,11 @@ namespace {
 using namespace ops;
 
 constexpr int kStages = 4;
+// CTA barrier (stage release) after every plane (1) or every second plane
+// (2: both stages consumed since the last barrier are re-armed together)
+#ifndef SB_RKPAIR_BARRIER_EVERY
+#define SB_RKPAIR_BARRIER_EVERY 2
+#endif
 enum { PAIR_A = 0, PAIR_B = 1, PAIR_LA = 2, PAIR_LB = 3 };
 
 __host__ __device__ constexpr int n_halo(int pair) { return pair == PAIR_A || pair == PAIR_LA ? 2 : pair == PAIR_B ? 3 : 4; }
@@ -268,8 +273,18 @@ __device__ __forceinline__ bool pair_plane(int i, const PCtx &c, const PairParam
         }
     }
 
+#if SB_RKPAIR_BARRIER_EVERY == 2
+    if ((i & 1) || i + 1 == c.nplanes) {   // uniform: every second plane, and the last
+        named_bar(1, c.nthr);              // every thread is done with the stages of planes <= i
+        if (c.tid == 0) {
+            if ((i & 1) && i - 1 + kStages < c.nplanes) issue<PAIR, TX>(c, P, i - 1 + kStages, (i - 1) & (kStages - 1));
+            if (i + kStages < c.nplanes) issue<PAIR, TX>(c, P, i + kStages, s);
+        }
+    }
+#else
     named_bar(1, c.nthr);   // every thread is done with stage s
     if (c.tid == 0 && i + kStages < c.nplanes) issue<PAIR, TX>(c, P, i + kStages, s);
+#endif
     if (i < 4) return false;
 
     constexpr int K0 = (R + 1) % 5, K1 = (R + 2) % 5, K2 = (R + 3) % 5, K3 = (R + 4) % 5, K4 = R;
