@@ -75,24 +75,33 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Wait for phase `parity` of an mbarrier.  A wait that has not completed
-// after ~2^24 polls traps (turns a pipeline bug into a launch error instead
-// of a hung GPU).
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    uint32_t done = 0;
-    for (uint32_t n = 0;; ++n) {
-        asm volatile(
-            "{\n"
-            ".reg .pred p;\n"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-            "selp.u32 %0, 1, 0, p;\n"
-            "}\n"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-        if (done) return;
+// One bounded hardware wait for phase `parity` of an mbarrier.
+__device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return done != 0;
+}
+
+// Out of line: keep retrying; a wait that has not completed after ~2^24
+// polls traps (turns a pipeline bug into a launch error instead of a hung
+// GPU).
+static __device__ __noinline__ void mbar_wait_slow(uint64_t *bar, uint32_t parity) {
+    for (uint32_t n = 0; !mbar_try(bar, parity); ++n)
         if (n > (1u << 24)) __trap();
-    }
+}
+
+// Wait for phase `parity` of an mbarrier: the common case (data already
+// there, or arriving within the hardware's wait window) is one try_wait.
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    if (__builtin_expect(!mbar_try(bar, parity), 0)) mbar_wait_slow(bar, parity);
 }
 
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *m) {
