@@ -120,12 +120,26 @@ def _declare(lib) -> None:
         fn.restype = res
 
 
+def library_path() -> Path:
+    """The library this process uses: ``STENCIL_B200_LIB`` if set; else the
+    tolerance-mode build (FMA contraction, ``libstencil_b200_fma.so``) when
+    ``STENCIL_B200_MODE=fma``; else the bit-exact product library."""
+    if os.environ.get("STENCIL_B200_LIB"):
+        return Path(os.environ["STENCIL_B200_LIB"])
+    mode = os.environ.get("STENCIL_B200_MODE", "exact")
+    if mode == "fma":
+        return Path(LIB_PATH).with_name("libstencil_b200_fma.so")
+    if mode != "exact":
+        raise UsageError(f"STENCIL_B200_MODE must be 'exact' or 'fma', not {mode!r}")
+    return Path(LIB_PATH)
+
+
 def load(path: str | os.PathLike | None = None):
     """Load (once) and return the library; raises if it is missing."""
     global _lib
     with _lock:
         if _lib is None:
-            p = Path(path) if path else Path(os.environ.get("STENCIL_B200_LIB", LIB_PATH))
+            p = Path(path) if path else library_path()
             if not p.exists():
                 raise DeviceError(f"{p} not built; run __graft_entry__.build() (no CPU fallback exists)")
             lib = C.CDLL(str(p))

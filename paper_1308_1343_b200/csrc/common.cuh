@@ -15,9 +15,16 @@
 namespace sb {
 
 // ---- exact-order fp64 arithmetic -------------------------------------------
+#if SB_FMA
+// tolerance mode (experiment): plain operators, contractible into FMAs with -fmad=true
+__device__ __forceinline__ double add(double a, double b) { return a + b; }
+__device__ __forceinline__ double sub(double a, double b) { return a - b; }
+__device__ __forceinline__ double mul(double a, double b) { return a * b; }
+#else
 __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+#endif
 
 // Unscaled 4th-order first difference: (u[-2] - u[+2]) + 8*(u[+1] - u[-1]).
 __device__ __forceinline__ double d1u(double m2, double m1, double p1, double p2) {
