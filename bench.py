@@ -90,18 +90,30 @@ class ClockSampler:
         except Exception:  # noqa: BLE001
             self._nv = None
 
-    def _run(self):
+    def sample(self):
         nv = self._nv
+        try:
+            self.mhz.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            for bit, name in self.REASONS.items():
+                if r & bit:
+                    self.reasons.add(name)
+        except Exception:  # noqa: BLE001
+            pass
+
+    def _run(self):
         while not self._stop.is_set():
-            try:
-                self.mhz.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
-                for bit, name in self.REASONS.items():
-                    if r & bit:
-                        self.reasons.add(name)
-            except Exception:  # noqa: BLE001
-                pass
+            self.sample()
             time.sleep(self.period)
+
+    def wait(self, event) -> None:
+        """Sample from the calling thread until `event` (recorded at the end
+        of the timed work) completes: the samples fall inside the timed
+        region even when the background thread gets little time."""
+        while not event.query():
+            if self._nv is not None:
+                self.sample()
+            time.sleep(0.001)
 
     def __enter__(self):
         if self._nv is not None:
@@ -270,6 +282,7 @@ def run_ours(args) -> None:
         for i in range(args.steps):
             prob.run(params)
             ev[i + 1].record(stream)
+        clk.wait(ev[-1])
         torch.cuda.synchronize()
     barrier()
     per = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
@@ -289,6 +302,7 @@ def run_ours(args) -> None:
             for _ in range(args.sustained_steps):
                 prob.run(params)
             s1.record(stream)
+            clk_s.wait(s1)
             torch.cuda.synchronize()
         barrier()
         s_ms = max_over_ranks(s0.elapsed_time(s1)) / args.sustained_steps
