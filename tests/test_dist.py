@@ -10,6 +10,7 @@ import oracle
 from paper_1308_1343_b200 import inputs
 from paper_1308_1343_b200.level import Box, box_difference
 from paper_1308_1343_b200.shard import shard_boxes, split_z
+from conftest import free_port
 
 
 def level(n):
@@ -76,7 +77,7 @@ def test_gloo_world2_level_sweep_matches_single_process():
     n, g, world = 24, 2, 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + os.getpid() % 1000
+    port = free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, n, g, q)) for r in range(world)]
     for p in procs:
         p.start()
@@ -112,7 +113,7 @@ def test_bench_under_torchrun_two_ranks(impl):
     import sys
     from pathlib import Path
     root = Path(__file__).resolve().parent.parent
-    port = 29400 + os.getpid() % 300 + (0 if impl == "ours" else 300)
+    port = free_port()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port), str(root / "bench.py"), "--gpus", "2",
            "--steps", "3", "--warmup", "3", "--impl", impl]

@@ -10,6 +10,7 @@ import oracle
 from paper_1308_1343_b200 import inputs
 from paper_1308_1343_b200.errors import UsageError
 from paper_1308_1343_b200.halo import z_cuts
+from conftest import free_port
 
 
 def test_z_cuts():
@@ -78,7 +79,7 @@ def test_two_ranks_ipc_on_one_gpu(schedule):
     _build.build()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29700 + os.getpid() % 200
+    port = free_port()
     procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q, schedule)) for r in range(2)]
     for p in procs:
         p.start()
