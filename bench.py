@@ -216,7 +216,7 @@ def run_ours(args) -> None:
     from paper_1308_1343_b200.configs import C2FourthOrder
     from paper_1308_1343_b200.tuner import LaunchParams
 
-    if rank == 0 or not _build.LIB.exists():
+    if local == 0:          # one builder per node; the other ranks wait, then load its library
         _build.build()
     if dist:
         dist.barrier()
