@@ -6,7 +6,8 @@ _update_rows style, static thread split over all host cores).
 
 GPU: median of CUDA-event timings of back-to-back launches at the kernels'
 default (swept) launch shapes, inputs resident in HBM (config 1: launches
-replayed from a CUDA graph — it is launch-bound).  CPU: a bounded sample of each workload
+replayed from a CUDA graph — it is launch-bound), with the SM clock and
+clock-event reasons sampled through NVML while timing.  CPU: a bounded sample of each workload
 (stated per row), timed with perf_counter, all host threads.
 """
 from __future__ import annotations
@@ -134,16 +135,19 @@ def main():
     threads = host_threads()
     cpu = {1: cpu_c1, 2: cpu_c2, 3: cpu_c3, 4: cpu_c4, 5: cpu_c5}
     rows = []
+    sys.path.insert(0, str(ROOT))
+    from bench import ClockSampler   # NVML SM clock + clock-event reasons while timing
     for k, cls in CONFIGS.items():
         prob = cls().setup()
-        t = gpu_time(prob, reps=100 if k == 1 else (20 if k != 5 else 5), graph=(k == 1))
+        with ClockSampler(torch.cuda.current_device()) as clk:
+            t = gpu_time(prob, reps=100 if k == 1 else (20 if k != 5 else 5), graph=(k == 1))
         gpts = prob.updates / t / 1e9
         cpu_pts, sample = cpu[k](threads, args.cpu_seconds)
         rows.append({"config": k, "name": cls.name, "gpu_s": t, "gpu_gpts": gpts,
                      "algorithmic_bytes": prob.canonical_bytes, "algorithmic_gbs": prob.canonical_bytes / t / 1e9,
                      "frac_of_measured_copy": prob.canonical_bytes / t / 1e9 / copy_peak,
                      "cpu_gpts": cpu_pts / 1e9, "cpu_sample": sample, "cpu_threads": threads,
-                     "gpu_over_cpu": gpts / (cpu_pts / 1e9)})
+                     "gpu_over_cpu": gpts / (cpu_pts / 1e9), "clocks": clk.summary()})
         del prob
         torch.cuda.empty_cache()
     print(json.dumps({"gpu": torch.cuda.get_device_name(0), "host_threads": threads,
