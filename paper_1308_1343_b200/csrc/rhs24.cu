@@ -39,19 +39,19 @@ constexpr int NV = SB_N_VARS, NT = SB_N_TERMS;
 constexpr int NSTAGE = 5;                               // planes resident: zc .. z+2
 constexpr int NTHREADS = NV * 32;                       // 768
 
-// One polynomial term: coefficient and the byte offsets of v_p (low 16 bits)
-// and v_q (high 16 bits) in the [240][32] operand array.
-struct __align__(16) Term {
-    double c;
-    uint32_t pq;
-    uint32_t pad;
-};
-constexpr size_t SMEM_BYTES = 128 + sizeof(Term) * NV * NT +
+// One polynomial term is 12 bytes: the coefficient's two 32-bit words and
+// the byte offsets of v_p (low 16 bits) and v_q (high 16 bits) in the
+// [240][32] operand array.  Packed, four terms are three 16-byte words, so
+// a warp fetches four terms with three broadcast LDS.128 (three shared-memory
+// wavefronts instead of four).
+constexpr int TW = NT * 3 / 4;                          // 16-byte words per output's table
+static_assert(NT % 4 == 0, "terms are fetched four at a time");
+constexpr size_t SMEM_BYTES = 128 + sizeof(uint4) * NV * TW +
                               sizeof(double) * ((size_t)NSTAGE * NV * PLANE + (size_t)3 * NV * HYc * TXc +
                                                 (size_t)10 * NV * NCOL);
 
 struct PolyConst {
-    Term t[NV][NT];
+    uint4 w[NV][TW];
 };
 __constant__ PolyConst g_poly;
 
@@ -67,7 +67,7 @@ struct Rhs24Params {
 
 struct Ctx {
     uint64_t *full;          // NSTAGE mbarriers
-    const Term *terms;       // [NV][NT] copy of the table in shared memory (broadcast reads)
+    const uint4 *terms;      // [NV][TW] copy of the packed table in shared memory (broadcast reads)
     double *ring;            // [NSTAGE][NV][PLANE]
     double *rxb;             // [3][NV][HYc][TXc]
     double *vals;            // [240][NCOL]
@@ -158,23 +158,22 @@ __device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c,
 
     // ---- phase B: output o = warp for the 32 columns of plane zc ----
     {
-        const Term *tt = c.terms + c.warp * NT;
+        const uint4 *tt = c.terms + c.warp * TW;
         const char *vb = reinterpret_cast<const char *>(c.vals + c.lane);
         auto V = [vb](uint32_t off) { return *reinterpret_cast<const double *>(vb + off); };
-        // one 16-byte broadcast load per term: (c, pq | pad)
-        auto T = [tt](int k, double &cf, uint32_t &pq) {
-            const double2 raw = *reinterpret_cast<const double2 *>(tt + k);
-            cf = raw.x;
-            pq = (uint32_t)__double_as_longlong(raw.y);
+        auto term = [&V](uint32_t lo, uint32_t hi, uint32_t pq) {
+            return mul(mul(__hiloint2double((int)hi, (int)lo), V(pq & 0xffffu)), V(pq >> 16));
         };
-        double cf;
-        uint32_t pq;
-        T(0, cf, pq);
-        double acc = mul(mul(cf, V(pq & 0xffffu)), V(pq >> 16));
-#pragma unroll 16
-        for (int k = 1; k < NT; ++k) {
-            T(k, cf, pq);
-            acc = add(acc, mul(mul(cf, V(pq & 0xffffu)), V(pq >> 16)));
+        double acc = 0.0;
+#pragma unroll 4
+        for (int g = 0; g < NT / 4; ++g) {
+            // three broadcast 16-byte loads carry terms 4g .. 4g+3
+            const uint4 a = tt[3 * g], b = tt[3 * g + 1], d = tt[3 * g + 2];
+            const double t0 = term(a.x, a.y, a.z);
+            acc = g == 0 ? t0 : add(acc, t0);
+            acc = add(acc, term(a.w, b.x, b.y));
+            acc = add(acc, term(b.z, b.w, d.x));
+            acc = add(acc, term(d.y, d.z, d.w));
         }
         if (c.active) {
             const int zc = c.Z0 - 4 + i;
@@ -189,9 +188,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) rhs24_kernel(const __grid_constan
     extern __shared__ __align__(1024) unsigned char smem[];
     Ctx c;
     c.full = reinterpret_cast<uint64_t *>(smem);
-    Term *terms = reinterpret_cast<Term *>(smem + 128);
+    uint4 *terms = reinterpret_cast<uint4 *>(smem + 128);
     c.terms = terms;
-    c.ring = reinterpret_cast<double *>(terms + NV * NT);
+    c.ring = reinterpret_cast<double *>(terms + NV * TW);
     c.rxb = c.ring + NSTAGE * NV * PLANE;
     c.vals = c.rxb + 3 * NV * HYc * TXc;
     c.tid = threadIdx.x;
@@ -219,7 +218,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rhs24_kernel(const __grid_constan
         fence_mbar_init();
         for (int j = 0; j < NSTAGE && j < c.nplanes; ++j) issue(P, c, j);
     }
-    for (int e = c.tid; e < NV * NT; e += NTHREADS) terms[e] = (&g_poly.t[0][0])[e];
+    for (int e = c.tid; e < NV * TW; e += NTHREADS) terms[e] = (&g_poly.w[0][0])[e];
     __syncthreads();
 
     Rings rg;
@@ -262,15 +261,19 @@ int launch_rhs24(const sb_array *in, const sb_array *out, const sb_space &sp, co
 
     std::lock_guard<std::mutex> lock(g_poly_mutex);
     static PolyConst host;
-    for (int o = 0; o < NV; ++o)
+    for (int o = 0; o < NV; ++o) {
+        uint32_t *words = reinterpret_cast<uint32_t *>(host.w[o]);   // 3 words per term
         for (int t = 0; t < NT; ++t) {
             const int pi = poly.p[o * NT + t], qi = poly.q[o * NT + t];
             if (pi < 0 || pi >= 10 * NV || qi < 0 || qi >= 10 * NV)
                 return fail(SB_USAGE, "rhs24: polynomial input index outside 0..239");
-            host.t[o][t].c = poly.coef[o * NT + t];
-            host.t[o][t].pq = (uint32_t)(pi * NCOL * 8) | ((uint32_t)(qi * NCOL * 8) << 16);
-            host.t[o][t].pad = 0;
+            uint64_t bits;
+            memcpy(&bits, &poly.coef[o * NT + t], sizeof bits);
+            words[3 * t] = (uint32_t)bits;
+            words[3 * t + 1] = (uint32_t)(bits >> 32);
+            words[3 * t + 2] = (uint32_t)(pi * NCOL * 8) | ((uint32_t)(qi * NCOL * 8) << 16);
         }
+    }
     const uint64_t fp = fnv1a(&host, sizeof(host), 1469598103934665603ULL);
     if (!g_poly_valid || fp != g_poly_fp) {
         int rc = check_cuda(cudaMemcpyToSymbolAsync(g_poly, &host, sizeof(host), 0, cudaMemcpyHostToDevice, st),
