@@ -39,13 +39,15 @@ constexpr int NV = SB_N_VARS, NT = SB_N_TERMS;
 constexpr int NSTAGE = 5;                               // planes resident: zc .. z+2
 constexpr int NTHREADS = NV * 32;                       // 768
 
-// One polynomial term is 12 bytes: the coefficient's two 32-bit words and
-// the byte offsets of v_p (low 16 bits) and v_q (high 16 bits) in the
-// [240][32] operand array.  Packed, four terms are three 16-byte words, so
-// a warp fetches four terms with three broadcast LDS.128 (three shared-memory
-// wavefronts instead of four).
-constexpr int TW = NT * 3 / 4;                          // 16-byte words per output's table
-static_assert(NT % 4 == 0, "terms are fetched four at a time");
+// One polynomial term is 10 bytes: the coefficient and a 16-bit operand
+// pair, p in the low byte and q in the high byte (both < 240; a row of the
+// [240][32] operand array is 256 bytes, so the byte offsets are p << 8 and
+// q << 8).  Eight terms pack into five 16-byte words — four of coefficient
+// pairs, one of the eight operand pairs — so a warp fetches eight terms with
+// five broadcast LDS.128 (five shared-memory wavefronts instead of eight).
+constexpr int TW = NT / 8 * 5;                          // 16-byte words per output's table
+static_assert(NT % 8 == 0, "terms are fetched eight at a time");
+static_assert(NCOL * 8 == 256, "operand offsets are row index << 8");
 constexpr size_t SMEM_BYTES = 128 + sizeof(uint4) * NV * TW +
                               sizeof(double) * ((size_t)NSTAGE * NV * PLANE + (size_t)3 * NV * HYc * TXc +
                                                 (size_t)10 * NV * NCOL);
@@ -161,19 +163,26 @@ __device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c,
         const uint4 *tt = c.terms + c.warp * TW;
         const char *vb = reinterpret_cast<const char *>(c.vals + c.lane);
         auto V = [vb](uint32_t off) { return *reinterpret_cast<const double *>(vb + off); };
-        auto term = [&V](uint32_t lo, uint32_t hi, uint32_t pq) {
-            return mul(mul(__hiloint2double((int)hi, (int)lo), V(pq & 0xffffu)), V(pq >> 16));
-        };
+        // pq: p in bits 0-7, q in bits 8-15 -> byte offsets p << 8, q << 8
+        auto term = [&V](double cf, uint32_t pq) { return mul(mul(cf, V((pq << 8) & 0xff00u)), V(pq & 0xff00u)); };
         double acc = 0.0;
-#pragma unroll 4
-        for (int g = 0; g < NT / 4; ++g) {
-            // three broadcast 16-byte loads carry terms 4g .. 4g+3
-            const uint4 a = tt[3 * g], b = tt[3 * g + 1], d = tt[3 * g + 2];
-            const double t0 = term(a.x, a.y, a.z);
+#pragma unroll 2
+        for (int g = 0; g < NT / 8; ++g) {
+            // five broadcast 16-byte loads carry terms 8g .. 8g+7
+            const double2 c01 = *reinterpret_cast<const double2 *>(tt + 5 * g);
+            const double2 c23 = *reinterpret_cast<const double2 *>(tt + 5 * g + 1);
+            const double2 c45 = *reinterpret_cast<const double2 *>(tt + 5 * g + 2);
+            const double2 c67 = *reinterpret_cast<const double2 *>(tt + 5 * g + 3);
+            const uint4 o = tt[5 * g + 4];
+            const double t0 = term(c01.x, o.x & 0xffffu);
             acc = g == 0 ? t0 : add(acc, t0);
-            acc = add(acc, term(a.w, b.x, b.y));
-            acc = add(acc, term(b.z, b.w, d.x));
-            acc = add(acc, term(d.y, d.z, d.w));
+            acc = add(acc, term(c01.y, o.x >> 16));
+            acc = add(acc, term(c23.x, o.y & 0xffffu));
+            acc = add(acc, term(c23.y, o.y >> 16));
+            acc = add(acc, term(c45.x, o.z & 0xffffu));
+            acc = add(acc, term(c45.y, o.z >> 16));
+            acc = add(acc, term(c67.x, o.w & 0xffffu));
+            acc = add(acc, term(c67.y, o.w >> 16));
         }
         if (c.active) {
             const int zc = c.Z0 - 4 + i;
@@ -261,19 +270,19 @@ int launch_rhs24(const sb_array *in, const sb_array *out, const sb_space &sp, co
 
     std::lock_guard<std::mutex> lock(g_poly_mutex);
     static PolyConst host;
-    for (int o = 0; o < NV; ++o) {
-        uint32_t *words = reinterpret_cast<uint32_t *>(host.w[o]);   // 3 words per term
-        for (int t = 0; t < NT; ++t) {
-            const int pi = poly.p[o * NT + t], qi = poly.q[o * NT + t];
-            if (pi < 0 || pi >= 10 * NV || qi < 0 || qi >= 10 * NV)
-                return fail(SB_USAGE, "rhs24: polynomial input index outside 0..239");
-            uint64_t bits;
-            memcpy(&bits, &poly.coef[o * NT + t], sizeof bits);
-            words[3 * t] = (uint32_t)bits;
-            words[3 * t + 1] = (uint32_t)(bits >> 32);
-            words[3 * t + 2] = (uint32_t)(pi * NCOL * 8) | ((uint32_t)(qi * NCOL * 8) << 16);
+    for (int o = 0; o < NV; ++o)
+        for (int g = 0; g < NT / 8; ++g) {
+            double *cf = reinterpret_cast<double *>(&host.w[o][5 * g]);          // 8 coefficients
+            uint16_t *pq = reinterpret_cast<uint16_t *>(&host.w[o][5 * g + 4]);  // 8 operand pairs
+            for (int k = 0; k < 8; ++k) {
+                const int t = 8 * g + k;
+                const int pi = poly.p[o * NT + t], qi = poly.q[o * NT + t];
+                if (pi < 0 || pi >= 10 * NV || qi < 0 || qi >= 10 * NV)
+                    return fail(SB_USAGE, "rhs24: polynomial input index outside 0..239");
+                cf[k] = poly.coef[o * NT + t];
+                pq[k] = (uint16_t)(pi | (qi << 8));
+            }
         }
-    }
     const uint64_t fp = fnv1a(&host, sizeof(host), 1469598103934665603ULL);
     if (!g_poly_valid || fp != g_poly_fp) {
         int rc = check_cuda(cudaMemcpyToSymbolAsync(g_poly, &host, sizeof(host), 0, cudaMemcpyHostToDevice, st),
