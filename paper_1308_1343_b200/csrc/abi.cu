@@ -8,6 +8,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.h"
@@ -111,6 +112,28 @@ int make_tmap(CUtensorMap *m, const sb_array &a, int bx, int by, int bz) {
         snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d) for box %dx%dx%d", (int)r, bx, by, bz);
         return fail(SB_CUDA, buf);
     }
+    return SB_OK;
+}
+
+namespace {
+struct SmemLimit {
+    const void *fn;
+    int device, bytes;
+};
+std::mutex g_smem_mutex;
+std::vector<SmemLimit> g_smem_limits;
+}  // namespace
+
+int ensure_smem_limit(const void *fn, int bytes, const char *what) {
+    int dev = 0;
+    int rc = check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lock(g_smem_mutex);
+    for (const SmemLimit &l : g_smem_limits)
+        if (l.fn == fn && l.device == dev && l.bytes >= bytes) return SB_OK;
+    rc = check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), what);
+    if (rc) return rc;
+    g_smem_limits.push_back({fn, dev, bytes});
     return SB_OK;
 }
 

@@ -428,14 +428,7 @@ int launch_mode_ty(const D4Params &P, int nblocks, cudaStream_t st) {
     const int threads = (TX / NP) * P.ty;
     const size_t smem = smem_bytes(MODE, TX, P.ty);
     auto fn = d4_kernel<MODE, TX, NP, TYC>;
-    // raise the dynamic shared-memory limit once per instantiation (keeps the
-    // launch path free of non-stream calls, e.g. during CUDA-graph capture)
-    static int configured = 0;
-    if ((int)smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(d4)");
-        configured = 227 * 1024;
-    }
+    if (int rc = ensure_smem_limit((const void *)fn, 227 * 1024, "cudaFuncSetAttribute(d4)")) return rc;
     fn<<<nblocks, threads, smem, st>>>(P);
     return check_cuda(cudaGetLastError(), "d4_kernel launch");
 }

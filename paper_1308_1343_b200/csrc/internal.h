@@ -14,6 +14,12 @@ namespace sb {
 int fail(int code, const std::string &msg);
 int check_cuda(cudaError_t e, const char *what);
 
+// Raise kernel fn's dynamic shared-memory limit to `bytes` once per (kernel,
+// device): the attribute is per device, so a process that drives several
+// GPUs sets it on each; later calls are a lookup (no CUDA call, so the launch
+// path stays free of non-stream calls during CUDA-graph capture).
+int ensure_smem_limit(const void *fn, int bytes, const char *what);
+
 // Build a 3-D tiled TMA descriptor over the ghosted grid `a` whose boxes are
 // (bx, by, bz) elements.  Coordinates of interior (0,0,0) in the map are
 // (a.xpad, a.ghost, a.ghost).

@@ -242,10 +242,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) rhs24_kernel(const __grid_constan
     }
 }
 
-// Content fingerprint of the last uploaded table (uploads are stream-ordered);
-// the host staging copy and the fingerprint are shared, so guarded.
-uint64_t g_poly_fp = 0;
-bool g_poly_valid = false;
+// Content fingerprint of the last table uploaded to each device's
+// __constant__ bank (uploads are stream-ordered); the host staging copy and
+// the fingerprints are shared, so guarded.
+constexpr int kMaxDevices = 64;
+uint64_t g_poly_fp[kMaxDevices] = {};
+bool g_poly_valid[kMaxDevices] = {};
 std::mutex g_poly_mutex;
 
 uint64_t fnv1a(const void *data, size_t n, uint64_t h) {
@@ -284,15 +286,18 @@ int launch_rhs24(const sb_array *in, const sb_array *out, const sb_space &sp, co
             }
         }
     const uint64_t fp = fnv1a(&host, sizeof(host), 1469598103934665603ULL);
-    if (!g_poly_valid || fp != g_poly_fp) {
+    int dev = 0;
+    if (int rc = check_cuda(cudaGetDevice(&dev), "cudaGetDevice")) return rc;
+    if (dev < 0 || dev >= kMaxDevices) return fail(SB_RESOURCE, "rhs24: device ordinal beyond the table cache");
+    if (!g_poly_valid[dev] || fp != g_poly_fp[dev]) {
         int rc = check_cuda(cudaMemcpyToSymbolAsync(g_poly, &host, sizeof(host), 0, cudaMemcpyHostToDevice, st),
                             "upload polynomial table");
         if (rc) return rc;
         // the staging copy must outlive the async upload
         rc = check_cuda(cudaStreamSynchronize(st), "synchronize polynomial upload");
         if (rc) return rc;
-        g_poly_fp = fp;
-        g_poly_valid = true;
+        g_poly_fp[dev] = fp;
+        g_poly_valid[dev] = true;
     }
 
     Rhs24Params P;
@@ -321,13 +326,8 @@ int launch_rhs24(const sb_array *in, const sb_array *out, const sb_space &sp, co
     P.k11 = k.k11;
     const long long nblocks = (long long)P.ntx * P.nty * ntz;
     if (nblocks > 0x7fffffffLL) return fail(SB_RESOURCE, "rhs24: too many tiles");
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e =
-            cudaFuncSetAttribute(rhs24_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-        if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(rhs24)");
-        configured = true;
-    }
+    if (int rc = ensure_smem_limit((const void *)rhs24_kernel, (int)SMEM_BYTES, "cudaFuncSetAttribute(rhs24)"))
+        return rc;
     rhs24_kernel<<<(unsigned)nblocks, NTHREADS, SMEM_BYTES, st>>>(P);
     return check_cuda(cudaGetLastError(), "rhs24_kernel launch");
 }

@@ -433,12 +433,7 @@ size_t pair_smem(int pair, int tx, int ty) {
 template <int PAIR, int TX, int NP, int TYC>
 int launch_pair_ty(const PairParams &P, int nblocks, cudaStream_t st) {
     auto fn = rkpair_kernel<PAIR, TX, NP, TYC>;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return check_cuda(e, "cudaFuncSetAttribute(rkpair)");
-        configured = true;
-    }
+    if (int rc = ensure_smem_limit((const void *)fn, 227 * 1024, "cudaFuncSetAttribute(rkpair)")) return rc;
     fn<<<nblocks, (TX / NP) * P.ty, pair_smem(PAIR, TX, P.ty), st>>>(P);
     return check_cuda(cudaGetLastError(), "rkpair_kernel launch");
 }
