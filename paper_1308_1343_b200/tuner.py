@@ -335,6 +335,33 @@ def _valid_unique(space, p, cand, setup, topo) -> list:
     return out
 
 
+# Module-level forms of the reference's plan-space functions, same names and
+# signatures (tuner.py:130, 190, 212, 221, 297), over the CPU plan space;
+# pinned against the reference by tests/golden/tuner_golden.json.
+_PLAN_SPACE = PlanSpace()
+
+
+def check_params(p: ExecParams, setup: LoopSetup, topo: TopologyConfig) -> None:
+    """Raise UsageError unless p satisfies every invariant for this setup."""
+    _PLAN_SPACE.check(p, setup, topo)
+
+
+def enumerate_valid_params(setup: LoopSetup, topo: TopologyConfig) -> list[ExecParams]:
+    return _PLAN_SPACE.enumerate(setup, topo)
+
+
+def random_params(setup: LoopSetup, topo: TopologyConfig, rng: random.Random) -> ExecParams:
+    return _PLAN_SPACE.random(setup, topo, rng)
+
+
+def params_initial(setup: LoopSetup, topo: TopologyConfig) -> ExecParams:
+    return _PLAN_SPACE.initial(setup, topo)
+
+
+def neighbors(p: ExecParams, setup: LoopSetup, topo: TopologyConfig) -> list[ExecParams]:
+    return _PLAN_SPACE.neighbors(p, setup, topo)
+
+
 # -- the device launch space ---------------------------------------------------
 
 @dataclass(frozen=True)

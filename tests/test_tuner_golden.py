@@ -1,0 +1,69 @@
+"""The tuner against the reference's own outputs (tests/golden/tuner_golden.json,
+made by tests/golden/make_tuner_golden.py from stencilrt.tuner): the plan-space
+functions (tuner.py:130-346) give the same initial point, the same ordered
+neighbour and enumeration lists and the same random draws, and the state
+machine (tuner.py:371-487) walks the same parameter sequence and writes the
+same CSV log, byte for byte."""
+import hashlib
+import json
+import random
+from pathlib import Path
+
+import pytest
+
+from paper_1308_1343_b200 import tuner as T
+from paper_1308_1343_b200.tunesim import BowlSurface
+
+GOLDEN = json.loads((Path(__file__).parent / "golden" / "tuner_golden.json").read_text())
+
+
+def _flat(p) -> list:
+    return [list(p.coarse_split), list(p.tile_size), list(p.fine_split), p.vector_width]
+
+
+def _sha(lines) -> str:
+    return hashlib.sha256("\n".join(lines).encode()).hexdigest()
+
+
+def test_plan_space_matches_reference():
+    n_err = 0
+    for case in GOLDEN["plan_space"]:
+        setup = T.LoopSetup("k", tuple(case["extents"]), case["alignment"], case["n_coarse"], case["n_fine"])
+        topo = T.TopologyConfig(lane_width=case["lane_width"])
+        if "initial_error" in case:
+            # the reference raises UsageError / ResourceError; ours are the same classes by name
+            with pytest.raises(Exception) as ei:
+                T.params_initial(setup, topo)
+            assert type(ei.value).__name__ == case["initial_error"]
+            n_err += 1
+            continue
+        p0 = T.params_initial(setup, topo)
+        assert _flat(p0) == case["initial"], case
+        T.check_params(p0, setup, topo)
+        nb = [json.dumps(_flat(q)) for q in T.neighbors(p0, setup, topo)]
+        assert (len(nb), _sha(nb)) == (case["neighbors_count"], case["neighbors_sha256"]), case
+        en = [json.dumps(_flat(q)) for q in T.enumerate_valid_params(setup, topo)]
+        assert (len(en), _sha(en)) == (case["enumerate_count"], case["enumerate_sha256"]), case
+        assert [_flat(T.random_params(setup, topo, random.Random(s))) for s in range(3)] == case["random"]
+    assert len(GOLDEN["plan_space"]) == 360
+
+
+@pytest.mark.parametrize("case", GOLDEN["trajectories"], ids=lambda c: f"{c['extents']}-s{c['seed']}")
+def test_tuner_trajectory_and_log_match_reference(case, tmp_path):
+    surf = BowlSurface()
+    tu = T.Tuner(T.TopologyConfig(lane_width=case["lane_width"], rng_seed=case["seed"],
+                                  n_coarse_threads=case["n_coarse"], n_fine_threads=case["n_fine"]))
+    setup = T.LoopSetup("k", tuple(case["extents"]), "vector", case["n_coarse"], case["n_fine"])
+    seq = []
+    for _ in range(case["rounds"]):
+        p = tu.next_params(setup)
+        seq.append(p.flat())
+        tu.record_timing(setup, p, surf.cost(p))
+    assert seq[:12] == case["first"] and seq[-3:] == case["last"]
+    assert _sha(seq) == case["params_sha256"]
+    log = tmp_path / "log.csv"
+    tu.write_log(log)
+    assert hashlib.sha256(log.read_bytes()).hexdigest() == case["log_sha256"]
+    best, best_t = tu.best(setup)
+    assert best.flat() == case["best"] and best_t == case["best_time"]
+    assert tu.phase(setup) == case["phase"]
