@@ -67,3 +67,14 @@ def test_tuner_trajectory_and_log_match_reference(case, tmp_path):
     best, best_t = tu.best(setup)
     assert best.flat() == case["best"] and best_t == case["best_time"]
     assert tu.phase(setup) == case["phase"]
+
+
+def test_build_plan_pieces_match_reference():
+    from paper_1308_1343_b200.traverse import IndexSpace, build_plan
+    for case in GOLDEN["plans"]:
+        cs, ts, fs, w = case["params"]
+        p = T.ExecParams(tuple(cs), tuple(ts), tuple(fs), w)
+        pieces = [json.dumps([list(x.lo), list(x.hi)])
+                  for x in build_plan(IndexSpace(tuple(case["lo"]), tuple(case["hi"])), p).pieces()]
+        assert (len(pieces), _sha(pieces)) == (case["pieces_count"], case["pieces_sha256"]), case
+    assert len(GOLDEN["plans"]) > 500
