@@ -102,7 +102,11 @@ int make_tmap(CUtensorMap *m, const sb_array &a, int bx, int by, int bz) {
     cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
     cuuint32_t estr[3] = {1, 1, 1};
 #ifndef SB_TMA_L2_PROMOTION
-#define SB_TMA_L2_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+// 128-byte L2 promotion: a staged row (TX + 4 doubles) is 288 bytes for the
+// default 32-wide tiles, so 256-byte granules over-fetch at row ends
+// (level Laplacian -0.5 %, the other kernels unchanged:
+// profiles/r01/v16_ab_l2_policy.log)
+#define SB_TMA_L2_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_L2_128B
 #endif
     CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, SB_TMA_L2_PROMOTION,

@@ -133,7 +133,11 @@ __device__ __forceinline__ void issue_plane(const Ctx &c, const D4Params &P, con
     const bool with_pw = NPW > 0 && j >= 4;
     const uint32_t bytes = (uint32_t)((TX + 4) * c.H * 8 + (with_pw ? NPW * TX * c.TY * 8 : 0));
     mbar_arrive_expect_tx(&c.full[s], bytes);
-    tma_load_3d(st, &B.tmap, B.tma0[0] + c.X0 - 2, B.tma0[1] + c.Y0 - 2, B.tma0[2] + c.Z0 - 2 + j, &c.full[s]);
+    if constexpr (all10(MODE))   // ten output streams: keep the (11x smaller) input resident for its re-reads
+        tma_load_3d_hint(st, &B.tmap, B.tma0[0] + c.X0 - 2, B.tma0[1] + c.Y0 - 2, B.tma0[2] + c.Z0 - 2 + j, &c.full[s],
+                         l2_policy_evict_last());
+    else
+        tma_load_3d(st, &B.tmap, B.tma0[0] + c.X0 - 2, B.tma0[1] + c.Y0 - 2, B.tma0[2] + c.Z0 - 2 + j, &c.full[s]);
     if constexpr (NPW > 0) {
         if (with_pw) {
             const int zc = c.Z0 - 4 + j;
