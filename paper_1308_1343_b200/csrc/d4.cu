@@ -347,6 +347,8 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
 template <int MODE, int TX, int NP, int TYC>
 __global__ void __launch_bounds__(lb_threads(MODE, TX, NP, TYC), lb_minb(MODE, TYC))
     d4_kernel(const __grid_constant__ D4Params P) {
+    pdl_launch_dependents();    // PDL: see lap7.cu
+    pdl_wait_prerequisites();
     constexpr int TPR = TX / NP;    // threads per row
     constexpr int W = TX + 4;       // smem row width (elements)
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -433,8 +435,7 @@ int launch_mode_ty(const D4Params &P, int nblocks, cudaStream_t st) {
     const size_t smem = smem_bytes(MODE, TX, P.ty);
     auto fn = d4_kernel<MODE, TX, NP, TYC>;
     if (int rc = ensure_smem_limit((const void *)fn, 227 * 1024, "cudaFuncSetAttribute(d4)")) return rc;
-    fn<<<nblocks, threads, smem, st>>>(P);
-    return check_cuda(cudaGetLastError(), "d4_kernel launch");
+    return launch_pdl(fn, dim3(nblocks), dim3(threads), smem, st, "d4_kernel launch", P);
 }
 
 template <int MODE, int TX, int NP>

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <string>
+#include <utility>
 
 #include "../../include/stencil_b200.h"
 
@@ -19,6 +20,28 @@ int check_cuda(cudaError_t e, const char *what);
 // GPUs sets it on each; later calls are a lookup (no CUDA call, so the launch
 // path stays free of non-stream calls during CUDA-graph capture).
 int ensure_smem_limit(const void *fn, int bytes, const char *what);
+
+// Launch `kernel` with programmatic stream serialization allowed (PDL): it
+// may start while the previous kernel on `st` drains and must itself wait
+// (griddepcontrol.wait, pdl_wait_prerequisites) before touching memory.
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, const char *what,
+               Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+#ifndef SB_PDL
+#define SB_PDL 1
+#endif
+    cfg.numAttrs = SB_PDL ? 1 : 0;
+    return check_cuda(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), what);
+}
 
 // Build a 3-D tiled TMA descriptor over the ghosted grid `a` whose boxes are
 // (bx, by, bz) elements.  Coordinates of interior (0,0,0) in the map are

@@ -107,6 +107,11 @@ __device__ __forceinline__ void lap7_column(const Grid &dst, const Grid &src, in
 
 __global__ void __launch_bounds__(256) lap7_kernel(Grid dst, Grid src, int lo0, int lo1, int lo2, int hi0,
                                                    int hi1, int hi2, int ax0, int zc, double c0, double c1) {
+    // Programmatic dependent launch: the next sweep of a back-to-back loop may
+    // be scheduled now; this one touches memory only once the previous
+    // kernel on the stream has completed (a no-op without such a predecessor).
+    pdl_launch_dependents();
+    pdl_wait_prerequisites();
     const int x = ax0 + (blockIdx.x * 32 + threadIdx.x) * 2;
     const int y = lo1 + blockIdx.y * blockDim.y + threadIdx.y;
     const int z0 = lo2 + blockIdx.z * zc;
@@ -175,9 +180,8 @@ int launch_lap7(const sb_array &dst, const sb_array &src, const sb_space &sp, do
     const int pairs = (sp.hi[0] - ax0 + 1) / 2;
     dim3 block(32, ty);
     dim3 grid((pairs + 31) / 32, (sp.hi[1] - sp.lo[1] + ty - 1) / ty, (sp.hi[2] - sp.lo[2] + zc - 1) / zc);
-    lap7_kernel<<<grid, block, 0, st>>>(grid_of(dst), grid_of(src), sp.lo[0], sp.lo[1], sp.lo[2], sp.hi[0],
-                                        sp.hi[1], sp.hi[2], ax0, zc, c0, c1);
-    return check_cuda(cudaGetLastError(), "lap7_kernel launch");
+    return launch_pdl(lap7_kernel, grid, block, 0, st, "lap7_kernel launch", grid_of(dst), grid_of(src), sp.lo[0],
+                      sp.lo[1], sp.lo[2], sp.hi[0], sp.hi[1], sp.hi[2], ax0, zc, c0, c1);
 }
 
 int launch_lap7_iterate(const sb_array &a, const sb_array &b, const sb_space &sp, double c0, double c1, int iters,

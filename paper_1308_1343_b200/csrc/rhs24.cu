@@ -194,6 +194,8 @@ __device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c,
 }
 
 __global__ void __launch_bounds__(NTHREADS, 1) rhs24_kernel(const __grid_constant__ Rhs24Params P) {
+    pdl_launch_dependents();    // PDL: see lap7.cu
+    pdl_wait_prerequisites();
     extern __shared__ __align__(1024) unsigned char smem[];
     Ctx c;
     c.full = reinterpret_cast<uint64_t *>(smem);
@@ -328,8 +330,7 @@ int launch_rhs24(const sb_array *in, const sb_array *out, const sb_space &sp, co
     if (nblocks > 0x7fffffffLL) return fail(SB_RESOURCE, "rhs24: too many tiles");
     if (int rc = ensure_smem_limit((const void *)rhs24_kernel, (int)SMEM_BYTES, "cudaFuncSetAttribute(rhs24)"))
         return rc;
-    rhs24_kernel<<<(unsigned)nblocks, NTHREADS, SMEM_BYTES, st>>>(P);
-    return check_cuda(cudaGetLastError(), "rhs24_kernel launch");
+    return launch_pdl(rhs24_kernel, dim3((unsigned)nblocks), dim3(NTHREADS), SMEM_BYTES, st, "rhs24_kernel launch", P);
 }
 
 }  // namespace sb

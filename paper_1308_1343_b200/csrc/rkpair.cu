@@ -360,6 +360,8 @@ __device__ __forceinline__ bool pair_plane(int i, const PCtx &c, const PairParam
 template <int PAIR, int TX, int NP, int TYC>
 __global__ void __launch_bounds__(lb_threads(TX, NP, TYC), lb_minb(PAIR, TYC))
     rkpair_kernel(const __grid_constant__ PairParams P) {
+    pdl_launch_dependents();    // PDL: see lap7.cu
+    pdl_wait_prerequisites();
     constexpr int TPR = TX / NP;
     constexpr int W = TX + 4;
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -434,8 +436,8 @@ template <int PAIR, int TX, int NP, int TYC>
 int launch_pair_ty(const PairParams &P, int nblocks, cudaStream_t st) {
     auto fn = rkpair_kernel<PAIR, TX, NP, TYC>;
     if (int rc = ensure_smem_limit((const void *)fn, 227 * 1024, "cudaFuncSetAttribute(rkpair)")) return rc;
-    fn<<<nblocks, (TX / NP) * P.ty, pair_smem(PAIR, TX, P.ty), st>>>(P);
-    return check_cuda(cudaGetLastError(), "rkpair_kernel launch");
+    return launch_pdl(fn, dim3(nblocks), dim3((TX / NP) * P.ty), pair_smem(PAIR, TX, P.ty), st,
+                      "rkpair_kernel launch", P);
 }
 
 template <int PAIR, int TX, int NP>
