@@ -31,7 +31,7 @@ from .tuner import LaunchParams, LaunchSpace
 D4_ALL_SPACE = LaunchSpace(kind="d4_all", max_threads_pair=256, max_threads_scalar=512, rx_buffer=True)
 D4_SPACE = LaunchSpace(kind="lap4", max_threads_pair=512, max_threads_scalar=512)
 RK4_SPACE = LaunchSpace(kind="rk4", max_threads_pair=256, max_threads_scalar=512)
-LAP7_SPACE = LaunchSpace(kind="lap7", max_threads_pair=256, radius=1, stages=0, tile_xs=(64,),
+LAP7_SPACE = LaunchSpace(kind="lap7", max_threads_pair=256, radius=1, stages=0, tile_xs=(64,), z_min=1,
                          tile_ys=(1, 2, 4, 8), points=(2,))
 
 

@@ -382,6 +382,7 @@ class LaunchSpace:
     stages: int = 4
     tile_xs: tuple[int, ...] = (32, 64, 128)
     tile_ys: tuple[int, ...] = (1, 2, 4, 8, 16, 32)
+    z_min: int = 4              # smallest z chunk (powers of two from here, then the whole extent)
 
     def smem_bytes(self, tx: int, ty: int) -> int:
         w, h = tx + 2 * self.radius, ty + 2 * self.radius
@@ -390,7 +391,7 @@ class LaunchSpace:
         return 128 + self.stages * stage + extra
 
     def _z_values(self, nz: int) -> list[int]:
-        vals, z = [], 4
+        vals, z = [], self.z_min
         while z < nz:
             vals.append(z)
             z *= 2
