@@ -26,7 +26,11 @@
  *    reference's unfused-FMA contract, vlanes.py:33 / vlanes.py:243-249.
  *  - All launches are asynchronous on the caller's stream (a cudaStream_t
  *    passed as void*; NULL = legacy default stream).  No entry point
- *    allocates or frees caller memory.
+ *    allocates or frees caller memory.  Kernels are launched with
+ *    programmatic stream serialization (programmatic dependent launch): a
+ *    sweep may be scheduled while the previous kernel on the stream drains,
+ *    but it reads or writes memory only after that kernel has completed, so
+ *    stream order is preserved exactly as for a plain launch.
  *  - Return codes: SB_OK, SB_USAGE (contract violation, maps to the
  *    reference's UsageError, lattice.py:22), SB_RESOURCE (ResourceError,
  *    lattice.py:26), SB_CUDA (CUDA failure).  sb_last_error() returns a
