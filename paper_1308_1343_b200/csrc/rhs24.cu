@@ -15,11 +15,13 @@
 //     (plane loop unrolled five ways), the x differences of the plane
 //     (with halo rows) into a 3-plane shared ring for Dxy; two planes later
 //     the ten slots of the completed plane go to a [240][32] shared array;
-//   * phase B — warp o evaluates output o for the 32 columns: every lane runs
-//     the same term, so (c, p, q) is one broadcast 16-byte shared-memory read
-//     (the table is copied to shared memory per CTA: 24 warps walking 24
-//     different 1 KB slices of __constant__ memory thrash the constant cache)
-//     and the two operand loads per term are conflict-free rows of [240][32].
+//   * phase B — half-warp h of warp w (w < 12) evaluates output 2w + h for
+//     the 32 columns, two per lane: the half-warp runs the same term, so the
+//     packed (c, p, q) words are broadcast 16-byte shared-memory reads that
+//     serve two outputs per LDS.128 (the table is copied to shared memory per
+//     CTA: 24 warps walking 24 different 1 KB slices of __constant__ memory
+//     thrash the constant cache), and the two operand loads per term are
+//     conflict-free 16-byte reads of rows of [240][32].
 // Two CTA barriers per plane.  Bound: shared-memory bandwidth (two 8-byte
 // operand loads per term per point), then the FP64 pipe.
 #include <cstring>
@@ -75,7 +77,6 @@ struct Ctx {
     double *vals;            // [240][NCOL]
     int tid, warp, lane, cx, cy;
     int X0, Y0, Z0, Z1, nplanes;
-    bool active;
 };
 
 struct Rings {
@@ -158,36 +159,49 @@ __device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c,
     if (c.tid == 0 && freed >= 0 && freed + NSTAGE < c.nplanes) issue(P, c, freed + NSTAGE);
     if (!out_plane) return false;
 
-    // ---- phase B: output o = warp for the 32 columns of plane zc ----
-    {
-        const uint4 *tt = c.terms + c.warp * TW;
-        const char *vb = reinterpret_cast<const char *>(c.vals + c.lane);
-        auto V = [vb](uint32_t off) { return *reinterpret_cast<const double *>(vb + off); };
-        // pq: p in bits 0-7, q in bits 8-15 -> byte offsets p << 8, q << 8
-        auto term = [&V](double cf, uint32_t pq) { return mul(mul(cf, V((pq << 8) & 0xff00u)), V(pq & 0xff00u)); };
-        double acc = 0.0;
+    // ---- phase B: warps 0..11, half-warp h of warp w evaluates output 2w + h
+    // for the 32 columns of plane zc, two adjacent columns per lane ----
+    // Every lane of a half-warp runs the same term, so a table word is a
+    // broadcast within the half-warp and one LDS.128 (two half-warp phases)
+    // serves two outputs: half the table wavefronts of one output per warp,
+    // while the 16-byte operand loads move the same bytes per point.
+    if (c.warp < NV / 2) {
+        const int o = 2 * c.warp + (c.lane >> 4), l16 = c.lane & 15;
+        const uint4 *tt = c.terms + o * TW;
+        const char *vb = reinterpret_cast<const char *>(c.vals) + 16 * l16;
+        auto V = [vb](uint32_t off) { return *reinterpret_cast<const double2 *>(vb + off); };
+        double a0 = 0.0, a1 = 0.0;
+        // pq: p in bits 0-7, q in bits 8-15 -> byte offsets p << 8, q << 8 of the operand rows
+        auto term = [&](double cf, uint32_t pq, bool first) {
+            const double2 vp = V((pq << 8) & 0xff00u), vq = V(pq & 0xff00u);
+            const double t0 = mul(mul(cf, vp.x), vq.x), t1 = mul(mul(cf, vp.y), vq.y);
+            a0 = first ? t0 : add(a0, t0);
+            a1 = first ? t1 : add(a1, t1);
+        };
 #pragma unroll 2
         for (int g = 0; g < NT / 8; ++g) {
-            // five broadcast 16-byte loads carry terms 8g .. 8g+7
+            // five 16-byte loads carry terms 8g .. 8g+7 (eight coefficients, eight operand pairs)
             const double2 c01 = *reinterpret_cast<const double2 *>(tt + 5 * g);
             const double2 c23 = *reinterpret_cast<const double2 *>(tt + 5 * g + 1);
             const double2 c45 = *reinterpret_cast<const double2 *>(tt + 5 * g + 2);
             const double2 c67 = *reinterpret_cast<const double2 *>(tt + 5 * g + 3);
-            const uint4 o = tt[5 * g + 4];
-            const double t0 = term(c01.x, o.x & 0xffffu);
-            acc = g == 0 ? t0 : add(acc, t0);
-            acc = add(acc, term(c01.y, o.x >> 16));
-            acc = add(acc, term(c23.x, o.y & 0xffffu));
-            acc = add(acc, term(c23.y, o.y >> 16));
-            acc = add(acc, term(c45.x, o.z & 0xffffu));
-            acc = add(acc, term(c45.y, o.z >> 16));
-            acc = add(acc, term(c67.x, o.w & 0xffffu));
-            acc = add(acc, term(c67.y, o.w >> 16));
+            const uint4 w = tt[5 * g + 4];
+            term(c01.x, w.x & 0xffffu, g == 0);
+            term(c01.y, w.x >> 16, false);
+            term(c23.x, w.y & 0xffffu, false);
+            term(c23.y, w.y >> 16, false);
+            term(c45.x, w.z & 0xffffu, false);
+            term(c45.y, w.z >> 16, false);
+            term(c67.x, w.w & 0xffffu, false);
+            term(c67.y, w.w >> 16, false);
         }
-        if (c.active) {
-            const int zc = c.Z0 - 4 + i;
-            P.out[c.warp][(c.X0 + c.cx) + (long long)(c.Y0 + c.cy) * P.osy + (long long)zc * P.osz] = acc;
-        }
+        // vals column k was written by phase-A lane k: (x, y) = (k & 7, ((k >> 3) & 1) * 2 + (k >> 4));
+        // columns 2 l16 and 2 l16 + 1 are adjacent points of one row
+        const int k = 2 * l16;
+        const int x = c.X0 + (k & 7), y = c.Y0 + ((k >> 3) & 1) * 2 + (k >> 4), zc = c.Z0 - 4 + i;
+        const bool yin = y < P.hi[1];
+        store_pair(P.out[o] + x + (long long)y * P.osy + (long long)zc * P.osz, a0, a1,
+                   yin && x >= P.lo[0] && x < P.hi[0], yin && x + 1 >= P.lo[0] && x + 1 < P.hi[0]);
     }
     __syncthreads();   // the [240][32] array is rewritten by the next plane
     return false;
@@ -222,7 +236,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) rhs24_kernel(const __grid_constan
     c.Z0 = P.lo[2] + bz * P.zc;
     c.Z1 = min(c.Z0 + P.zc, P.hi[2]);
     c.nplanes = c.Z1 - c.Z0 + 4;
-    c.active = (c.X0 + c.cx >= P.lo[0]) && (c.X0 + c.cx < P.hi[0]) && (c.Y0 + c.cy < P.hi[1]);
 
     if (c.tid == 0) {
         for (int s = 0; s < NSTAGE; ++s) mbar_init(&c.full[s], 1);
