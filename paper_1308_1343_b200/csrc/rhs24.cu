@@ -9,12 +9,14 @@
 // One CTA = 24 warps owns an 8 x 4 tile of (x, y) columns and streams z:
 //   * every plane of all 24 fields (tile + 2-point halo, 12 x 8) arrives by
 //     TMA (24 cp.async.bulk.tensor.3d per plane, one mbarrier) into a
-//     6-stage shared-memory ring;
+//     3-stage shared-memory ring (a plane is read only in its own iteration);
 //   * phase A — warp v reduces field v, lane = column: u and the unscaled x/y
 //     first differences of the newest plane go into five-slot register rings
-//     (plane loop unrolled five ways), the x differences of the plane
-//     (with halo rows) into a 3-plane shared ring for Dxy; two planes later
-//     the ten slots of the completed plane go to a [240][32] shared array;
+//     (plane loop unrolled five ways), its in-plane second differences Dxx,
+//     Dyy into two-plane register queues (computed while its row and column
+//     values are in registers), the x differences of the plane (with halo
+//     rows) into a 3-plane shared ring for Dxy; two planes later the ten
+//     slots of the completed plane go to a [240][32] shared array;
 //   * phase B — half-warp h of warp w (w < 12) evaluates output 2w + h for
 //     the 32 columns, two per lane: the half-warp runs the same term, so the
 //     packed (c, p, q) words are broadcast 16-byte shared-memory reads that
@@ -38,7 +40,10 @@ constexpr int TXc = 8, TYc = 4, NCOL = TXc * TYc;      // 32 columns per CTA
 constexpr int HXc = TXc + 4, HYc = TYc + 4;             // 12 x 8 halo plane
 constexpr int PLANE = HXc * HYc;                        // 96 doubles
 constexpr int NV = SB_N_VARS, NT = SB_N_TERMS;
-constexpr int NSTAGE = 5;                               // planes resident: zc .. z+2
+#ifndef SB_RHS24_NSTAGE
+#define SB_RHS24_NSTAGE 3
+#endif
+constexpr int NSTAGE = SB_RHS24_NSTAGE;                 // staged planes: the newest + NSTAGE-1 in flight
 constexpr int NTHREADS = NV * 32;                       // 768
 
 // One polynomial term is 10 bytes: the coefficient and a 16-bit operand
@@ -81,6 +86,7 @@ struct Ctx {
 
 struct Rings {
     double u[5], rx[5], ry[5];
+    double dxx[2], dyy[2];   // Dxx, Dyy of the two planes before the newest ([0]: z-1, [1]: z-2)
 };
 
 // Physical row of logical row r (0..7) of an 8-wide rx plane: parity pattern
@@ -108,6 +114,7 @@ __device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c,
     const int v = c.warp;   // phase A: this warp's field
     mbar_wait(&c.full[s], (i / NSTAGE) & 1);
 
+    double dxx_new, dyy_new;
     // ---- phase A, newest plane z = Z0-2+i: u, rx, ry into the rings; rx plane (+ halo rows) ----
     {
         const double *pl = c.ring + (s * NV + v) * PLANE;
@@ -116,6 +123,10 @@ __device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c,
         rg.u[R] = row[2];
         rg.rx[R] = d1u(row[0], row[1], row[3], row[4]);
         rg.ry[R] = d1u(col[0], col[HXc], col[3 * HXc], col[4 * HXc]);
+        // the in-plane second differences of this plane now, while its row and
+        // column values are in registers (used two planes later)
+        dxx_new = d2(row[0], row[1], row[2], row[3], row[4], P.k2);
+        dyy_new = d2(col[0], col[HXc], row[2], col[3 * HXc], col[4 * HXc], P.k2);
         double *rxs = c.rxb + ((i % 3) * NV + v) * (HYc * TXc);
         rxs[rxrow(c.cy + 2) * TXc + c.cx] = rg.rx[R];
         // lanes double as the 4 halo rows x 8 columns; half-warps take rows {0, 6} and {1, 7}
@@ -130,10 +141,6 @@ __device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c,
     if (out_plane) {
         __syncwarp();    // rx plane of zc was written by this warp two planes ago; keep lanes in step
         constexpr int K0 = (R + 1) % 5, K1 = (R + 2) % 5, K2 = (R + 3) % 5, K3 = (R + 4) % 5, K4 = R;
-        const int sc = (i - 2) % NSTAGE;
-        const double *pl = c.ring + (sc * NV + v) * PLANE;
-        const double *row = pl + (c.cy + 2) * HXc + c.cx;
-        const double *col = pl + c.cy * HXc + c.cx + 2;
         const double uc = rg.u[K2];
         const double *rxs = c.rxb + (((i - 2) % 3) * NV + v) * (HYc * TXc) + c.cx;
         double *o = c.vals + (10 * v) * NCOL + c.lane;
@@ -141,8 +148,8 @@ __device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c,
         o[1 * NCOL] = mul(rg.rx[K2], P.k1);
         o[2 * NCOL] = mul(rg.ry[K2], P.k1);
         o[3 * NCOL] = mul(d1u(rg.u[K0], rg.u[K1], rg.u[K3], rg.u[K4]), P.k1);
-        o[4 * NCOL] = d2(row[0], row[1], uc, row[3], row[4], P.k2);
-        o[5 * NCOL] = d2(col[0], col[HXc], uc, col[3 * HXc], col[4 * HXc], P.k2);
+        o[4 * NCOL] = rg.dxx[1];
+        o[5 * NCOL] = rg.dyy[1];
         o[6 * NCOL] = d2(rg.u[K0], rg.u[K1], uc, rg.u[K3], rg.u[K4], P.k2);
         o[7 * NCOL] = mul(d1u(rxs[rxrow(c.cy + 0) * TXc], rxs[rxrow(c.cy + 1) * TXc], rxs[rxrow(c.cy + 3) * TXc],
                               rxs[rxrow(c.cy + 4) * TXc]),
@@ -151,12 +158,15 @@ __device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c,
         o[9 * NCOL] = mul(d1u(rg.ry[K0], rg.ry[K1], rg.ry[K3], rg.ry[K4]), P.k11);
     }
 
-    // every slot of plane zc is written; the stage of the oldest plane still
-    // held is no longer read: planes 0 and 1 (halo planes, phase A1 only) after
-    // their own iteration, plane i-2 after its slots at iteration i >= 4
+    rg.dxx[1] = rg.dxx[0];
+    rg.dxx[0] = dxx_new;
+    rg.dyy[1] = rg.dyy[0];
+    rg.dyy[0] = dyy_new;
+    // every slot of plane zc is written, and every staged plane is read only
+    // in its own iteration (phase A of the newest plane): stage s is free for
+    // plane i + NSTAGE
     __syncthreads();
-    const int freed = i < 2 ? i : (i >= 4 ? i - 2 : -1);
-    if (c.tid == 0 && freed >= 0 && freed + NSTAGE < c.nplanes) issue(P, c, freed + NSTAGE);
+    if (c.tid == 0 && i + NSTAGE < c.nplanes) issue(P, c, i + NSTAGE);
     if (!out_plane) return false;
 
     // ---- phase B: warps 0..11, half-warp h of warp w evaluates output 2w + h
@@ -248,6 +258,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rhs24_kernel(const __grid_constan
     Rings rg;
 #pragma unroll
     for (int k = 0; k < 5; ++k) rg.u[k] = rg.rx[k] = rg.ry[k] = 0.0;
+    rg.dxx[0] = rg.dxx[1] = rg.dyy[0] = rg.dyy[1] = 0.0;
     for (int i = 0;; i += 5) {
         if (plane<0>(i + 0, P, c, rg)) break;
         if (plane<1>(i + 1, P, c, rg)) break;
