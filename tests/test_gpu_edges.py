@@ -157,3 +157,38 @@ def test_random_levels_random_launches(seed):
         want = np.empty((nz, ny, nx))
         oracle.lap4(want, u, 2, (0, nx, 0, ny, 0, nz), p.k.k2)
         assert same(got, want), (b, tx, ty, pp)
+
+
+def test_d4_all_nonfinite_inputs_follow_ieee():
+    """NaN and +-Inf in the input propagate as in the reference's numpy
+    arithmetic: every finite output and every infinity is bit-identical, and
+    the outputs that are NaN on the host are NaN on the device (NaN payloads
+    are not part of the contract: x86 propagates the operand's payload, the
+    GPU returns the canonical quiet NaN)."""
+    from paper_1308_1343_b200.grid import DeviceGrid
+    from paper_1308_1343_b200.kernels import FourthOrderAll
+    from paper_1308_1343_b200.traverse import IndexSpace
+    ext = (40, 12, 9)
+    nx, ny, nz = ext
+    g = 2
+    rng = np.random.default_rng(99)
+    u = rng.uniform(-1, 1, (nz + 2 * g, ny + 2 * g, nx + 2 * g))
+    u[4, 6, 7] = np.nan
+    u[7, 3, 30] = np.inf
+    u[2, 10, 20] = -np.inf
+    u[5, 5, 41] = 1e308            # overflow to inf inside the stencil sums
+    k = inputs.D4Constants.for_spacing(1.0 / 17)
+    src = DeviceGrid(ext, g)
+    src.upload(u)
+    outs = [DeviceGrid(ext, 0).fill_(0.25) for _ in range(10)]
+    FourthOrderAll(outs, src, k).launch(IndexSpace((0, 0, 0), ext), LaunchParams(32, 4, 4, 2))
+    want = [np.empty((nz, ny, nx)) for _ in range(10)]
+    with np.errstate(all="ignore"):
+        oracle.d4_all(want, u, g, (0, nx, 0, ny, 0, nz), k)
+    for i in range(10):
+        got = outs[i].download()
+        nan_w, nan_g = np.isnan(want[i]), np.isnan(got)
+        assert nan_w.any()                    # the NaN reaches every derivative's stencil
+        assert np.array_equal(nan_w, nan_g), i
+        assert np.array_equal(got[~nan_g].view(np.uint64), want[i][~nan_w].view(np.uint64)), i
+        assert np.isinf(want[i]).any() == np.isinf(got).any(), i
