@@ -45,6 +45,10 @@ constexpr int NV = SB_N_VARS, NT = SB_N_TERMS;
 #endif
 constexpr int NSTAGE = SB_RHS24_NSTAGE;                 // staged planes: the newest + NSTAGE-1 in flight
 constexpr int NTHREADS = NV * 32;                       // 768
+#ifndef SB_RHS24_PHASEB_UNROLL
+#define SB_RHS24_PHASEB_UNROLL 8
+#endif
+constexpr int kPhaseBUnroll = SB_RHS24_PHASEB_UNROLL;  // eight-term groups per phase-B loop iteration
 
 // One polynomial term is 10 bytes: the coefficient and a 16-bit operand
 // pair, p in the low byte and q in the high byte (both < 240; a row of the
@@ -188,7 +192,7 @@ __device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c,
             a0 = first ? t0 : add(a0, t0);
             a1 = first ? t1 : add(a1, t1);
         };
-#pragma unroll 2
+#pragma unroll kPhaseBUnroll
         for (int g = 0; g < NT / 8; ++g) {
             // five 16-byte loads carry terms 8g .. 8g+7 (eight coefficients, eight operand pairs)
             const double2 c01 = *reinterpret_cast<const double2 *>(tt + 5 * g);
