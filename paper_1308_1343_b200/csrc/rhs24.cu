@@ -9,7 +9,7 @@
 // One CTA = 24 warps owns an 8 x 4 tile of (x, y) columns and streams z:
 //   * every plane of all 24 fields (tile + 2-point halo, 12 x 8) arrives by
 //     TMA (24 cp.async.bulk.tensor.3d per plane, one mbarrier) into a
-//     3-stage shared-memory ring (a plane is read only in its own iteration);
+//     2-stage shared-memory ring (a plane is read only in its own iteration);
 //   * phase A — warp v reduces field v, lane = column: u and the unscaled x/y
 //     first differences of the newest plane go into five-slot register rings
 //     (plane loop unrolled five ways), its in-plane second differences Dxx,
@@ -41,7 +41,7 @@ constexpr int HXc = TXc + 4, HYc = TYc + 4;             // 12 x 8 halo plane
 constexpr int PLANE = HXc * HYc;                        // 96 doubles
 constexpr int NV = SB_N_VARS, NT = SB_N_TERMS;
 #ifndef SB_RHS24_NSTAGE
-#define SB_RHS24_NSTAGE 3
+#define SB_RHS24_NSTAGE 2
 #endif
 constexpr int NSTAGE = SB_RHS24_NSTAGE;                 // staged planes: the newest + NSTAGE-1 in flight
 constexpr int NTHREADS = NV * 32;                       // 768
