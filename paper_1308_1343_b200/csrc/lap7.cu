@@ -7,6 +7,9 @@
 // neighbours through L1.  Expression tree (stencil.py:35-39):
 //   dst = C0*b + C1*(((xm + xp) + (ym + yp)) + (zm + zp))
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "common.cuh"
 #include "internal.h"
@@ -207,17 +210,27 @@ int launch_lap7_iterate(const sb_array &a, const sb_array &b, const sb_space &sp
     if (e != cudaSuccess) return check_cuda(e, "lap7_iterate occupancy");
     const int blocks = (int)std::min<long long>(ntiles, (long long)per_sm * sms);
 
-    // one arrival counter per device, owned by the library, zeroed on the stream
-    static unsigned *counters[64] = {};
-    if (dev < 0 || dev >= 64) return fail(SB_RESOURCE, "lap7_iterate: device index out of range");
-    if (!counters[dev] && (e = cudaMalloc(&counters[dev], sizeof(unsigned))) != cudaSuccess)
-        return check_cuda(e, "lap7_iterate counter");
-    if ((e = cudaMemsetAsync(counters[dev], 0, sizeof(unsigned), st)) != cudaSuccess)
+    // one arrival counter per (device, stream), owned by the library and
+    // zeroed on the stream: launches on one stream are ordered, so they can
+    // share it; launches on different streams may run concurrently and must not
+    unsigned *ctr_dev = nullptr;
+    {
+        static std::mutex mu;
+        static std::map<std::pair<int, cudaStream_t>, unsigned *> counters;
+        std::lock_guard<std::mutex> lock(mu);
+        unsigned *&slot = counters[{dev, st}];
+        if (!slot && (e = cudaMalloc(&slot, sizeof(unsigned))) != cudaSuccess) {
+            slot = nullptr;
+            return check_cuda(e, "lap7_iterate counter");
+        }
+        ctr_dev = slot;
+    }
+    if ((e = cudaMemsetAsync(ctr_dev, 0, sizeof(unsigned), st)) != cudaSuccess)
         return check_cuda(e, "lap7_iterate counter reset");
 
     Grid ga = grid_of(a), gb = grid_of(b);
     int lo0 = sp.lo[0], lo1 = sp.lo[1], lo2 = sp.lo[2], hi0 = sp.hi[0], hi1 = sp.hi[1], hi2 = sp.hi[2];
-    unsigned *ctr = counters[dev];
+    unsigned *ctr = ctr_dev;
     void *args[] = {&ga, &gb, &lo0, &lo1, &lo2, &hi0, &hi1, &hi2, (void *)&ax0, (void *)&zc, (void *)&gx,
                     (void *)&gy, (void *)&gz, &c0, &c1, &iters, &ctr};
     e = cudaLaunchCooperativeKernel((const void *)lap7_iterate_kernel, dim3(blocks), dim3(32, ty), args, 0, st);
