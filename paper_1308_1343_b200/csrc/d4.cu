@@ -11,7 +11,9 @@
 //     from HBM into a 4-stage shared-memory ring by TMA
 //     (cp.async.bulk.tensor.3d) with mbarrier completion; after the one
 //     CTA barrier per plane (all reads of that stage done) thread 0 re-arms
-//     the stage for plane i+4 — no producer warp, no spinning;
+//     the stage for plane i+4 — no producer warp, no spinning; the ten-output
+//     sweep loads its input with an L2 evict_last policy (the 11x larger .cs
+//     output stream would otherwise push out planes other CTAs re-read);
 //   * each thread owns NP (1 or 2) adjacent x points; x tiles are anchored on
 //     absolute multiples of TX, so pairs are 16-byte aligned and lanes outside
 //     [lo, hi) compute but never store (the iterate_masked frame rule,
