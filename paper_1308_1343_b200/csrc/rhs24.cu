@@ -6,18 +6,21 @@
 // polynomial  ((t_0 + t_1) + ...) + t_63,  t_k = (c_ok * v_p) * v_q
 // (oracle/stencils.py: rhs24).
 //
-// One CTA = 24 warps owns an 8 x 4 tile of (x, y) columns and streams z:
+// One CTA = 12 warps owns an 8 x 4 tile of (x, y) columns and streams z:
 //   * every plane of all 24 fields (tile + 2-point halo, 12 x 8) arrives by
 //     TMA (24 cp.async.bulk.tensor.3d per plane, one mbarrier) into a
 //     2-stage shared-memory ring (a plane is read only in its own iteration);
-//   * phase A — warp v reduces field v, lane = column: u and the unscaled x/y
+//   * phase A — warp w reduces fields w and w + 12 (SB_RHS24_FPW = 2; 160
+//     registers per thread, twice the independent work per warp, no idle
+//     warps in phase B; 24 warps of one field each: 80-register cap,
+//     4.5 % slower), lane = column: u and the unscaled x/y
 //     first differences of the newest plane go into five-slot register rings
 //     (plane loop unrolled five ways), its in-plane second differences Dxx,
 //     Dyy into two-plane register queues (computed while its row and column
 //     values are in registers), the x differences of the plane (with halo
 //     rows) into a 3-plane shared ring for Dxy; two planes later the ten
 //     slots of the completed plane go to a [240][32] shared array;
-//   * phase B — half-warp h of warp w (w < 12) evaluates output 2w + h for
+//   * phase B — half-warp h of warp w evaluates output 2w + h for
 //     the 32 columns, two per lane: the half-warp runs the same term, so the
 //     packed (c, p, q) words are broadcast 16-byte shared-memory reads that
 //     serve two outputs per LDS.128 (the table is copied to shared memory per
@@ -44,7 +47,12 @@ constexpr int NV = SB_N_VARS, NT = SB_N_TERMS;
 #define SB_RHS24_NSTAGE 2
 #endif
 constexpr int NSTAGE = SB_RHS24_NSTAGE;                 // staged planes: the newest + NSTAGE-1 in flight
-constexpr int NTHREADS = NV * 32;                       // 768
+#ifndef SB_RHS24_FPW
+#define SB_RHS24_FPW 2   // fields per warp in phase A (1: 24 warps, 2: 12 warps)
+#endif
+constexpr int FPW = SB_RHS24_FPW;
+constexpr int NWARPS = NV / FPW;
+constexpr int NTHREADS = NWARPS * 32;                   // 768 / 384
 #ifndef SB_RHS24_PHASEB_UNROLL
 #define SB_RHS24_PHASEB_UNROLL 8
 #endif
@@ -127,15 +135,17 @@ __device__ __forceinline__ void issue(const Rhs24Params &P, const Ctx &c, int j)
 }
 
 template <int R>
-__device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c, Rings &rg) {
+__device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c, Rings (&rgs)[FPW]) {
     if (i >= c.nplanes) return true;
     const int s = i % NSTAGE;
-    const int v = c.warp;   // phase A: this warp's field
     mbar_wait(&c.full[s], (i / NSTAGE) & 1);
 
-    double dxx_new, dyy_new;
+    double dxx_new[FPW], dyy_new[FPW];
     // ---- phase A, newest plane z = Z0-2+i: u, rx, ry into the rings; rx plane (+ halo rows) ----
-    {
+#pragma unroll
+    for (int f = 0; f < FPW; ++f) {
+        const int v = c.warp + f * NWARPS;   // this warp's field f
+        Rings &rg = rgs[f];
         const double *pl = c.ring + (s * NV + v) * PLANE;
         const double *col = pl + c.cy * HXc + c.cx + 2;
         double row[5];
@@ -145,8 +155,8 @@ __device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c,
         rg.ry[R] = d1u(col[0], col[HXc], col[3 * HXc], col[4 * HXc]);
         // the in-plane second differences of this plane now, while its row and
         // column values are in registers (used two planes later)
-        dxx_new = d2(row[0], row[1], row[2], row[3], row[4], P.k2);
-        dyy_new = d2(col[0], col[HXc], row[2], col[3 * HXc], col[4 * HXc], P.k2);
+        dxx_new[f] = d2(row[0], row[1], row[2], row[3], row[4], P.k2);
+        dyy_new[f] = d2(col[0], col[HXc], row[2], col[3 * HXc], col[4 * HXc], P.k2);
         double *rxs = c.rxb + ((i % 3) * NV + v) * (HYc * TXc);
         rxs[rxrow(c.cy + 2) * TXc + c.cx] = rg.rx[R];
         // lanes double as the 4 halo rows x 8 columns; half-warps take rows {0, 6} and {1, 7}
@@ -159,8 +169,12 @@ __device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c,
 
     // ---- phase A, completed plane zc = z-2: the ten slots ----
     const bool out_plane = i >= 4;
-    if (out_plane) {
-        __syncwarp();    // rx plane of zc was written by this warp two planes ago; keep lanes in step
+    if (out_plane) __syncwarp();    // rx plane of zc was written by this warp two planes ago; keep lanes in step
+#pragma unroll
+    for (int f = 0; f < FPW; ++f) {
+        if (!out_plane) break;
+        const int v = c.warp + f * NWARPS;
+        Rings &rg = rgs[f];
         constexpr int K0 = (R + 1) % 5, K1 = (R + 2) % 5, K2 = (R + 3) % 5, K3 = (R + 4) % 5, K4 = R;
         const double uc = rg.u[K2];
         const double *rxs = c.rxb + (((i - 2) % 3) * NV + v) * (HYc * TXc) + c.cx;
@@ -179,10 +193,13 @@ __device__ __forceinline__ bool plane(int i, const Rhs24Params &P, const Ctx &c,
         o[9 * NCOL] = mul(d1u(rg.ry[K0], rg.ry[K1], rg.ry[K3], rg.ry[K4]), P.k11);
     }
 
-    rg.dxx[1] = rg.dxx[0];
-    rg.dxx[0] = dxx_new;
-    rg.dyy[1] = rg.dyy[0];
-    rg.dyy[0] = dyy_new;
+#pragma unroll
+    for (int f = 0; f < FPW; ++f) {
+        rgs[f].dxx[1] = rgs[f].dxx[0];
+        rgs[f].dxx[0] = dxx_new[f];
+        rgs[f].dyy[1] = rgs[f].dyy[0];
+        rgs[f].dyy[0] = dyy_new[f];
+    }
     // every slot of plane zc is written, and every staged plane is read only
     // in its own iteration (phase A of the newest plane): stage s is free for
     // plane i + NSTAGE
@@ -276,10 +293,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) rhs24_kernel(const __grid_constan
     for (int e = c.tid; e < NV * TW; e += NTHREADS) terms[e] = (&g_poly.w[0][0])[e];
     __syncthreads();
 
-    Rings rg;
+    Rings rg[FPW];
 #pragma unroll
-    for (int k = 0; k < 5; ++k) rg.u[k] = rg.rx[k] = rg.ry[k] = 0.0;
-    rg.dxx[0] = rg.dxx[1] = rg.dyy[0] = rg.dyy[1] = 0.0;
+    for (int f = 0; f < FPW; ++f) {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) rg[f].u[k] = rg[f].rx[k] = rg[f].ry[k] = 0.0;
+        rg[f].dxx[0] = rg[f].dxx[1] = rg[f].dyy[0] = rg[f].dyy[1] = 0.0;
+    }
     for (int i = 0;; i += 5) {
         if (plane<0>(i + 0, P, c, rg)) break;
         if (plane<1>(i + 1, P, c, rg)) break;
