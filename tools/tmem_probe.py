@@ -1,0 +1,107 @@
+"""TMEM vs shared-memory operand feeds for the config-5 phase B
+(tools/csrc/tmem_probe.cu, built to tools/libtmem_probe.so):
+
+    nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -shared \\
+         -Xcompiler -fPIC tools/csrc/tmem_probe.cu -o tools/libtmem_probe.so
+    python tools/tmem_probe.py > profiles/r02/tmem_probe.json
+
+Prints raw tcgen05.ld bandwidth (bytes / clk / SM at the SM clock sampled
+during the run) and, for the phase-B loop on 128 points per CTA, point-terms
+per clock per SM, with the outputs checked bit for bit against numpy's
+((c * v_p) * v_q) summed left to right.
+"""
+import ctypes as C
+import json
+import statistics
+from pathlib import Path
+
+import numpy as np
+import torch
+
+lib = C.CDLL(str(Path(__file__).resolve().parent / "libtmem_probe.so"))
+lib.ldtm_launch.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
+lib.phaseb_launch.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p]
+sms = torch.cuda.get_device_properties(0).multi_processor_count
+st = torch.cuda.current_stream().cuda_stream
+
+
+def clock_mhz():
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(0)
+        return pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+    except Exception:  # noqa: BLE001
+        return 1965
+
+
+def timed(fn, reps=7):
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+    ev[0].record()
+    mhz = []
+    for i in range(reps):
+        fn()
+        ev[i + 1].record()
+    mhz.append(clock_mhz())
+    torch.cuda.synchronize()
+    return statistics.median(ev[i].elapsed_time(ev[i + 1]) for i in range(reps)) * 1e-3, statistics.median(mhz)
+
+
+res = {"sm_count": sms}
+out = torch.zeros(1 << 12, dtype=torch.int64, device="cuda")
+for n, k in ((2, 4), (2, 8), (2, 16), (4, 4), (4, 8), (8, 4), (8, 8)):
+    for warps in (4, 8, 16):
+        iters = 4096
+        s, mhz = timed(lambda: lib.ldtm_launch(n, k, out.data_ptr(), sms, warps * 32, iters, st))
+        assert torch.cuda.synchronize() is None
+        by = sms * warps * iters * k * n * 4 * 32
+        res[f"ldtm_x{n}_k{k}_w{warps}_B_per_clk_sm"] = by / s / sms / (mhz * 1e6)
+        res[f"ldtm_x{n}_k{k}_w{warps}_instr_per_clk_sm"] = sms * warps * iters * k / s / sms / (mhz * 1e6)
+
+# phase B
+NOPS, NOUT, NTERM, NPTS, NSM = 240, 24, 64, 128, 112
+rng = np.random.default_rng(7)
+ops = rng.uniform(0.9, 1.1, (NOPS, NPTS))
+tdt = np.dtype([("c", "<f8"), ("p", "<u4"), ("q", "<u4")])
+tab = np.zeros((NOUT, NTERM), dtype=tdt)
+tab["c"] = rng.standard_normal((NOUT, NTERM))
+tab["p"] = rng.integers(0, NOPS, (NOUT, NTERM))
+tab["q"] = rng.integers(0, NSM, (NOUT, NTERM))
+tab_smem = tab.copy()
+tab_smem["p"] = rng.integers(0, NSM, (NOUT, NTERM))
+tab_tm = tab.copy()
+tab_tm["p"] = rng.integers(0, 128, (NOUT, NTERM))
+
+
+def want_of(t):
+    w = np.empty((NOUT, NPTS))
+    for o in range(NOUT):
+        acc = None
+        for k in range(NTERM):
+            term = (t["c"][o, k] * ops[t["p"][o, k]]) * ops[t["q"][o, k]]
+            acc = term if acc is None else acc + term
+        w[o] = acc
+    return w
+
+
+d_ops = torch.from_numpy(ops).cuda()
+for src, t in ((0, tab), (1, tab), (2, tab_smem), (3, tab_tm), (4, tab_smem)):
+    want = want_of(t)
+    d_tab = torch.from_numpy(t.view(np.uint8).copy()).cuda()
+    for nw in (4, 8, 12, 16, 24):
+        d_out = torch.zeros((NOUT, NPTS), dtype=torch.float64, device="cuda")
+        reps = 64
+        rc = lib.phaseb_launch(src, nw, d_ops.data_ptr(), d_tab.data_ptr(), d_out.data_ptr(), sms, reps, st)
+        if rc == -1:
+            continue
+        torch.cuda.synchronize()
+        ok = d_out.cpu().numpy().tobytes() == want.tobytes()
+        s, mhz = timed(lambda: lib.phaseb_launch(src, nw, d_ops.data_ptr(), d_tab.data_ptr(), d_out.data_ptr(), sms,
+                                                 reps, st))
+        pt_terms = sms * reps * NOUT * NTERM * NPTS
+        res[f"phaseb_src{src}_w{nw}"] = {"point_terms_per_clk_sm": pt_terms / s / sms / (mhz * 1e6), "ms": s * 1e3,
+                                         "bits_ok": ok, "mhz": mhz}
+print(json.dumps(res, indent=1))
