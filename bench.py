@@ -85,10 +85,22 @@ class ClockSampler:
             import pynvml
             pynvml.nvmlInit()
             self._nv = pynvml
-            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._h = self._handle(pynvml, index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
         except Exception:  # noqa: BLE001
             self._nv = None
+
+    @staticmethod
+    def _handle(pynvml, index: int):
+        """NVML handle of CUDA device `index` by PCI bus id (NVML ignores
+        CUDA_VISIBLE_DEVICES and may order devices differently)."""
+        try:
+            import torch
+            p = torch.cuda.get_device_properties(index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:  # noqa: BLE001
+            return pynvml.nvmlDeviceGetHandleByIndex(index)
 
     def sample(self):
         nv = self._nv

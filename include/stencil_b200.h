@@ -174,7 +174,10 @@ SB_API int sb_lap7(sb_array dst, sb_array src, sb_space space, double c0, double
  * sweep k reads a and writes b for even k, the reverse for odd k, with a
  * grid-wide barrier between sweeps; the result is in b for odd `iters`, in
  * a for even.  Both grids need ghost >= 1 with the same (fixed) boundary
- * values.  Bit-identical to `iters` sb_lap7 calls. */
+ * values.  Bit-identical to `iters` sb_lap7 calls.  The grid barrier uses a
+ * library-owned 64-bit counter per (device, stream) from a pool that
+ * sb_init reserves; without a prior sb_init the first call on a device
+ * allocates the pool and is therefore refused inside a CUDA-graph capture. */
 SB_API int sb_lap7_iterate(sb_array a, sb_array b, sb_space space, double c0, double c1, int32_t iters,
                            sb_launch p, void *stream);
 

@@ -161,6 +161,20 @@ def call(name: str, *args) -> None:
     raise DeviceError(f"{name}: {msg} (status {rc})")
 
 
+_inited: set[int] = set()
+
+
+def init_current_device() -> None:
+    """sb_init on torch's current device, once per device (reserves the
+    library's per-device scratch, e.g. sb_lap7_iterate's barrier counters,
+    outside any CUDA-graph capture)."""
+    import torch
+    dev = torch.cuda.current_device()
+    if dev not in _inited:
+        call("sb_init", dev)
+        _inited.add(dev)
+
+
 def space(lo, hi) -> sb_space:
     s = sb_space()
     for d in range(3):

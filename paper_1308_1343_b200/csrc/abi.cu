@@ -154,7 +154,8 @@ const char *sb_last_error(void) { return t_last_error.c_str(); }
 int sb_init(int device) {
     int rc = check_cuda(cudaSetDevice(device), "cudaSetDevice");
     if (rc) return rc;
-    return check_cuda(cudaFree(nullptr), "context init");
+    if ((rc = check_cuda(cudaFree(nullptr), "context init"))) return rc;
+    return reserve_barrier_counters(device);
 }
 
 int sb_get_device_info(sb_device_info *info) {

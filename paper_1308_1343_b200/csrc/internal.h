@@ -53,6 +53,10 @@ int launch_lap7(const sb_array &dst, const sb_array &src, const sb_space &sp, do
                 const sb_launch &p, cudaStream_t st);
 int launch_lap7_iterate(const sb_array &a, const sb_array &b, const sb_space &sp, double c0, double c1, int iters,
                         const sb_launch &p, cudaStream_t st);
+// sb_lap7_iterate's grid-barrier counters (lap7.cu): reserve the device's
+// pool (sb_init), and the slot of a (device, stream) pair.
+int reserve_barrier_counters(int dev);
+int barrier_counter(int dev, cudaStream_t st, unsigned long long **out);
 int launch_diff1d(int kind, double *dst, const double *src, int n, cudaStream_t st);
 
 // RK stages: RK1 = stage 1, RK2 = stage 2 (acc_phi = pi0 + 2 pi_s: stage 1 never

@@ -121,17 +121,17 @@ __global__ void __launch_bounds__(256) lap7_kernel(Grid dst, Grid src, int lo0, 
     lap7_column<false>(dst, src, x, y, z0, min(z0 + zc, hi2), lo0, hi0, hi1, c0, c1);
 }
 
-// Grid-wide barrier of a cooperative (co-resident) launch: a monotone
+// Grid-wide barrier of a cooperative (co-resident) launch: a monotone 64-bit
 // arrival counter, zeroed before the launch; generation k completes when it
-// reaches k * gridDim.x.
-__device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned target) {
+// reaches k * gridDim.x (64 bits: no wrap for any int32 sweep count).
+__device__ __forceinline__ void grid_barrier(unsigned long long *ctr, unsigned long long target) {
     __syncthreads();
     if (threadIdx.x == 0 && threadIdx.y == 0) {
         __threadfence();
-        atomicAdd(ctr, 1u);
-        unsigned v;
+        atomicAdd(ctr, 1ull);
+        unsigned long long v;
         do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
         } while (v < target);
     }
     __syncthreads();
@@ -143,7 +143,7 @@ __device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned target) {
 // and meet at a grid barrier between sweeps — one launch for all sweeps.
 __global__ void __launch_bounds__(256) lap7_iterate_kernel(Grid a, Grid b, int lo0, int lo1, int lo2, int hi0, int hi1,
                                                            int hi2, int ax0, int zc, int gx, int gy, int gz,
-                                                           double c0, double c1, int iters, unsigned *ctr) {
+                                                           double c0, double c1, int iters, unsigned long long *ctr) {
     const int ntiles = gx * gy * gz;
     for (int it = 0; it < iters; ++it) {
         const Grid &src = (it & 1) ? b : a;
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(256) lap7_iterate_kernel(Grid a, Grid b, int l
             const int z0 = lo2 + tz * zc;
             lap7_column<true>(dst, src, x, y, z0, min(z0 + zc, hi2), lo0, hi0, hi1, c0, c1);
         }
-        if (it + 1 < iters) grid_barrier(ctr, (unsigned)(it + 1) * gridDim.x);
+        if (it + 1 < iters) grid_barrier(ctr, (unsigned long long)(it + 1) * gridDim.x);
     }
 }
 
@@ -171,6 +171,53 @@ __global__ void diff1d_kernel(int kind, double *dst, const double *src, int n) {
 }
 
 }  // namespace
+
+// Barrier counters of sb_lap7_iterate: a pool of kCounterPool 64-bit
+// counters per device, allocated by sb_init (reserve_barrier_counters) so a
+// first call inside a CUDA-graph capture needs no cudaMalloc; a (device,
+// stream) pair keeps its slot.  Without sb_init the pool is allocated on
+// first use, which is refused while the stream is capturing.
+namespace {
+constexpr int kCounterPool = 256;
+std::mutex g_ctr_mu;
+std::map<int, unsigned long long *> g_ctr_pool;                       // device -> pool
+std::map<std::pair<int, cudaStream_t>, unsigned long long *> g_ctr;  // (device, stream) -> slot
+std::map<int, int> g_ctr_used;
+
+int reserve_locked(int dev) {
+    if (g_ctr_pool.count(dev)) return SB_OK;
+    unsigned long long *pool = nullptr;
+    if (cudaError_t e = cudaMalloc(&pool, kCounterPool * sizeof(unsigned long long)); e != cudaSuccess)
+        return check_cuda(e, "barrier counter pool");
+    g_ctr_pool[dev] = pool;
+    g_ctr_used[dev] = 0;
+    return SB_OK;
+}
+}  // namespace
+
+int reserve_barrier_counters(int dev) {
+    std::lock_guard<std::mutex> lock(g_ctr_mu);
+    return reserve_locked(dev);
+}
+
+int barrier_counter(int dev, cudaStream_t st, unsigned long long **out) {
+    std::lock_guard<std::mutex> lock(g_ctr_mu);
+    auto it = g_ctr.find({dev, st});
+    if (it != g_ctr.end()) {
+        *out = it->second;
+        return SB_OK;
+    }
+    if (!g_ctr_pool.count(dev)) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+            return fail(SB_USAGE, "lap7_iterate: first use on this device inside a CUDA-graph capture; call sb_init first");
+        if (int rc = reserve_locked(dev)) return rc;
+    }
+    int &used = g_ctr_used[dev];
+    if (used >= kCounterPool) return fail(SB_RESOURCE, "lap7_iterate: more than 256 streams per device");
+    *out = g_ctr[{dev, st}] = g_ctr_pool[dev] + used++;
+    return SB_OK;
+}
 
 int launch_lap7(const sb_array &dst, const sb_array &src, const sb_space &sp, double c0, double c1,
                 const sb_launch &p, cudaStream_t st) {
@@ -213,24 +260,14 @@ int launch_lap7_iterate(const sb_array &a, const sb_array &b, const sb_space &sp
     // one arrival counter per (device, stream), owned by the library and
     // zeroed on the stream: launches on one stream are ordered, so they can
     // share it; launches on different streams may run concurrently and must not
-    unsigned *ctr_dev = nullptr;
-    {
-        static std::mutex mu;
-        static std::map<std::pair<int, cudaStream_t>, unsigned *> counters;
-        std::lock_guard<std::mutex> lock(mu);
-        unsigned *&slot = counters[{dev, st}];
-        if (!slot && (e = cudaMalloc(&slot, sizeof(unsigned))) != cudaSuccess) {
-            slot = nullptr;
-            return check_cuda(e, "lap7_iterate counter");
-        }
-        ctr_dev = slot;
-    }
-    if ((e = cudaMemsetAsync(ctr_dev, 0, sizeof(unsigned), st)) != cudaSuccess)
+    unsigned long long *ctr_dev = nullptr;
+    if (int rc = barrier_counter(dev, st, &ctr_dev)) return rc;
+    if ((e = cudaMemsetAsync(ctr_dev, 0, sizeof(unsigned long long), st)) != cudaSuccess)
         return check_cuda(e, "lap7_iterate counter reset");
 
     Grid ga = grid_of(a), gb = grid_of(b);
     int lo0 = sp.lo[0], lo1 = sp.lo[1], lo2 = sp.lo[2], hi0 = sp.hi[0], hi1 = sp.hi[1], hi2 = sp.hi[2];
-    unsigned *ctr = ctr_dev;
+    unsigned long long *ctr = ctr_dev;
     void *args[] = {&ga, &gb, &lo0, &lo1, &lo2, &hi0, &hi1, &hi2, (void *)&ax0, (void *)&zc, (void *)&gx,
                     (void *)&gy, (void *)&gz, &c0, &c1, &iters, &ctr};
     e = cudaLaunchCooperativeKernel((const void *)lap7_iterate_kernel, dim3(blocks), dim3(32, ty), args, 0, st);

@@ -30,7 +30,6 @@
 // Two CTA barriers per plane.  Bound: shared-memory bandwidth (two 8-byte
 // operand loads per term per point), then the FP64 pipe.
 #include <cstring>
-#include <mutex>
 
 #include "common.cuh"
 #include "internal.h"
@@ -67,16 +66,17 @@ constexpr int kPhaseBUnroll = SB_RHS24_PHASEB_UNROLL;  // eight-term groups per 
 constexpr int TW = NT / 8 * 5;                          // 16-byte words per output's table
 static_assert(NT % 8 == 0, "terms are fetched eight at a time");
 static_assert(NCOL * 8 == 256, "operand offsets are row index << 8");
+static_assert(sizeof(uint4) * NV * TW < 20 * 1024, "term table must fit the kernel parameter space with the maps");
 constexpr size_t SMEM_BYTES = 128 + sizeof(uint4) * NV * TW +
                               sizeof(double) * ((size_t)NSTAGE * NV * PLANE + (size_t)3 * NV * HYc * TXc +
                                                 (size_t)10 * NV * NCOL);
 
-struct PolyConst {
-    uint4 w[NV][TW];
-};
-__constant__ PolyConst g_poly;
-
 struct Rhs24Params {
+    // the packed term table travels with the launch (kernel parameter space,
+    // copied to shared memory by every CTA): a launch never depends on state
+    // another launch or stream may change, and a captured graph replays the
+    // table it was captured with
+    uint4 terms[NV][TW];
     CUtensorMap tmap[NV];
     double *out[NV];
     long long osy, osz;      // output strides (shared by all outputs)
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rhs24_kernel(const __grid_constan
         fence_mbar_init();
         for (int j = 0; j < NSTAGE && j < c.nplanes; ++j) issue(P, c, j);
     }
-    for (int e = c.tid; e < NV * TW; e += NTHREADS) terms[e] = (&g_poly.w[0][0])[e];
+    for (int e = c.tid; e < NV * TW; e += NTHREADS) terms[e] = (&P.terms[0][0])[e];
     __syncthreads();
 
     Rings rg[FPW];
@@ -309,23 +309,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) rhs24_kernel(const __grid_constan
     }
 }
 
-// Content fingerprint of the last table uploaded to each device's
-// __constant__ bank (uploads are stream-ordered); the host staging copy and
-// the fingerprints are shared, so guarded.
-constexpr int kMaxDevices = 64;
-uint64_t g_poly_fp[kMaxDevices] = {};
-bool g_poly_valid[kMaxDevices] = {};
-std::mutex g_poly_mutex;
-
-uint64_t fnv1a(const void *data, size_t n, uint64_t h) {
-    const unsigned char *b = static_cast<const unsigned char *>(data);
-    for (size_t i = 0; i < n; ++i) {
-        h ^= b[i];
-        h *= 1099511628211ULL;
-    }
-    return h;
-}
-
 }  // namespace
 
 int launch_rhs24(const sb_array *in, const sb_array *out, const sb_space &sp, const sb_d4_constants &k,
@@ -337,12 +320,12 @@ int launch_rhs24(const sb_array *in, const sb_array *out, const sb_space &sp, co
         if (out[v].sy != out[0].sy || out[v].sz != out[0].sz)
             return fail(SB_USAGE, "rhs24: all outputs must share row and plane strides");
 
-    std::lock_guard<std::mutex> lock(g_poly_mutex);
-    static PolyConst host;
+    Rhs24Params P;
+    memset(&P, 0, sizeof(P));
     for (int o = 0; o < NV; ++o)
         for (int g = 0; g < NT / 8; ++g) {
-            double *cf = reinterpret_cast<double *>(&host.w[o][5 * g]);          // 8 coefficients
-            uint16_t *pq = reinterpret_cast<uint16_t *>(&host.w[o][5 * g + 4]);  // 8 operand pairs
+            double *cf = reinterpret_cast<double *>(&P.terms[o][5 * g]);          // 8 coefficients
+            uint16_t *pq = reinterpret_cast<uint16_t *>(&P.terms[o][5 * g + 4]);  // 8 operand pairs
             for (int k = 0; k < 8; ++k) {
                 const int t = 8 * g + k;
                 const int pi = poly.p[o * NT + t], qi = poly.q[o * NT + t];
@@ -352,23 +335,6 @@ int launch_rhs24(const sb_array *in, const sb_array *out, const sb_space &sp, co
                 pq[k] = (uint16_t)(pi | (qi << 8));
             }
         }
-    const uint64_t fp = fnv1a(&host, sizeof(host), 1469598103934665603ULL);
-    int dev = 0;
-    if (int rc = check_cuda(cudaGetDevice(&dev), "cudaGetDevice")) return rc;
-    if (dev < 0 || dev >= kMaxDevices) return fail(SB_RESOURCE, "rhs24: device ordinal beyond the table cache");
-    if (!g_poly_valid[dev] || fp != g_poly_fp[dev]) {
-        int rc = check_cuda(cudaMemcpyToSymbolAsync(g_poly, &host, sizeof(host), 0, cudaMemcpyHostToDevice, st),
-                            "upload polynomial table");
-        if (rc) return rc;
-        // the staging copy must outlive the async upload
-        rc = check_cuda(cudaStreamSynchronize(st), "synchronize polynomial upload");
-        if (rc) return rc;
-        g_poly_fp[dev] = fp;
-        g_poly_valid[dev] = true;
-    }
-
-    Rhs24Params P;
-    memset(&P, 0, sizeof(P));
     for (int v = 0; v < NV; ++v) {
         int rc = make_tmap(&P.tmap[v], in[v], HXc, HYc, 1);
         if (rc) return rc;

@@ -96,6 +96,7 @@ class Laplacian7(DeviceKernel):
         (``sb_lap7_iterate``); returns the grid holding the result."""
         if a.extents != b.extents or a.lower != b.lower:
             raise UsageError("a and b must cover the same box")
+        _lib.init_current_device()
         _lib.call("sb_lap7_iterate", a.abi(), b.abi(), _local(space, a), self.c0, self.c1, int(iters),
                   _lib.launch_of(params or self.default_params, self.extra_flags), stream_ptr(stream))
         return b if iters % 2 else a
