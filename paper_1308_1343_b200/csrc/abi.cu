@@ -95,6 +95,16 @@ int check_cuda(cudaError_t e, const char *what) {
 int make_tmap(CUtensorMap *m, const sb_array &a, int bx, int by, int bz) {
     std::call_once(g_encode_once, resolve_encode);
     if (!g_encode) return fail(SB_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    // The driver-API encoder needs a current context.  A host thread whose
+    // first CUDA call this is (e.g. a worker thread of the reference's
+    // execute_plan / run_static, traverse.py:162-260) has none until the
+    // runtime binds the current device's primary context: do that once per
+    // thread (cudaSetDevice binds it on later device switches).
+    thread_local bool t_bound = false;
+    if (!t_bound) {
+        if (int rc = check_cuda(cudaFree(nullptr), "bind the primary context to this thread")) return rc;
+        t_bound = true;
+    }
     double *base = a.origin - a.xpad - (int64_t)a.ghost * a.sy - (int64_t)a.ghost * a.sz;
     if (!aligned16(base)) return fail(SB_USAGE, "TMA base (row start of the first ghost row) not 16-byte aligned");
     cuuint64_t dims[3] = {(cuuint64_t)a.sy, (cuuint64_t)(a.ny + 2 * a.ghost), (cuuint64_t)(a.nz + 2 * a.ghost)};
