@@ -10,13 +10,23 @@ HBM (CUDA events on the launching stream, max over ranks); `e2e` repeats
 the metric through the public API with the input copied from pinned host
 memory and all ten outputs copied back inside the timed region.
 
+The same line carries `extra`: configs 1, 3, 4 and 5 timed the same way
+(K steps after W warm-up steps, CUDA events, NVML clocks during each timed
+region), each with its own roofline, so every BASELINE.json config is
+observed by the driver's run.
+
 Multi-GPU (torchrun): every rank sweeps its own 256^3 box — independent
 units, no data-path collective — so scaling is weak; the only
 communication is a barrier and the max-over-ranks time.
 
-`--impl reference` times the reference's algorithm on the host cores: the
-CPU oracle port (oracle/, numpy expression trees in the reference's
-_update_rows style driven by its static thread split), rank 0 only.
+`--impl reference` times the reference's algorithm on the host cores, rank 0
+only: each step is one WHOLE 256^3 sweep of config 2, driven by the
+reference's own ``stencilrt.traverse.run_static`` (traverse.py:235-260, the
+unmodified package installed under baseline/_ref) over all host threads,
+with the oracle's numpy expression trees in the reference's _update_rows
+style as the piece kernel (the reference has no 4th-order kernel of its
+own); without baseline/_ref the oracle's restatement of run_static drives
+the same kernel.
 """
 from __future__ import annotations
 
@@ -33,6 +43,7 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+REF_PKG = ROOT / "baseline" / "_ref"
 
 METRIC = "stencil grid-pt updates/s (config 2: 4th-order 10-output sweep, 256^3 fp64)"
 UNIT = "Gpts/s"
@@ -55,6 +66,16 @@ def measured_peaks() -> dict:
     return {}
 
 
+def fp64_peak() -> float | None:
+    """Measured FP64 (unfused DADD/DMUL) ops/s of this B200 pool
+    (tools/pipe_ceiling.py, profiles/r01/pipe_ceiling.json)."""
+    p = ROOT / "profiles" / "r01" / "pipe_ceiling.json"
+    try:
+        return float(json.loads(p.read_text())["fp64_ops_per_s"])
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def ncu_traffic() -> float | None:
     """dram bytes (read+write) per d4_all launch from the committed ncu summary."""
     p = ROOT / "profiles" / "ncu_summary.json"
@@ -64,6 +85,29 @@ def ncu_traffic() -> float | None:
         d = json.loads(p.read_text())
         return float(d["d4_all"]["dram_bytes_per_launch"])
     except (ValueError, KeyError, TypeError):
+        return None
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_engine():
+    """The reference's own traverse module from baseline/_ref, or None."""
+    if not (REF_PKG / "stencilrt").is_dir():
+        return None
+    if str(REF_PKG) not in sys.path:
+        sys.path.insert(0, str(REF_PKG))
+    try:
+        import stencilrt.traverse
+        return stencilrt.traverse
+    except Exception:  # noqa: BLE001
         return None
 
 
@@ -125,7 +169,7 @@ class ClockSampler:
         while not event.query():
             if self._nv is not None:
                 self.sample()
-            time.sleep(0.001)
+            time.sleep(0.0005)
 
     def __enter__(self):
         if self._nv is not None:
@@ -144,69 +188,227 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.mhz)}
 
 
-class CpuOracle:
-    """The oracle port over z-slabs of config 2 with all host threads."""
+# ---------------------------------------------------------------------------
+# CPU side: the reference's algorithm on the host cores
+# ---------------------------------------------------------------------------
 
-    def __init__(self, planes: int = 8):
+class CpuC2:
+    """Config 2 on the host: the oracle's numpy expression trees (the
+    reference's _update_rows style) as a ``Kernel`` piece function, driven by
+    the reference's run_static (baseline/_ref) or the oracle's restatement."""
+
+    def __init__(self):
         import oracle
         from oracle.stencils import host_threads
         from paper_1308_1343_b200 import inputs
         self.oracle = oracle
-        self.n, self.g, self.planes = 256, 2, planes
+        self.n, self.g = 256, 2
         self.u = inputs.c2_field(self.n, self.g)
+        self.sha = inputs.sha256(self.u)
         self.k = inputs.D4Constants.for_spacing(1.0 / self.n)
         self.threads = host_threads()
-        self.outs = [np.empty((planes, self.n, self.n)) for _ in range(10)]
-        self.z = 0
+        self.outs = [np.empty((self.n, self.n, self.n)) for _ in range(10)]
+        self.engine = reference_engine()
 
-    def slab(self) -> float:
-        """One slab of `planes` z-planes (all ten outputs); returns seconds."""
-        n, g, P = self.n, self.g, self.planes
-        z0 = self.z
-        self.z = (self.z + P) % (n - P + 1)
+    def kernel(self, piece) -> None:
+        (x0, y0, z0), (x1, y1, z1) = piece.lo, piece.hi
+        self.oracle.d4_all(self.outs, self.u, self.g, (x0, x1, y0, y1, z0, z1), self.k)
 
-        def work(a, b):
-            ds = self.oracle.stencils.derivs9(self.u, g, (0, n, 0, n, z0 + a, z0 + b), self.k)
-            lap = (ds[3] + ds[4]) + ds[5]
-            for o, v in zip(self.outs, ds + [lap]):
-                o[a:b] = v
+    @property
+    def engine_name(self) -> str:
+        return ("stencilrt.traverse.run_static (reference, baseline/_ref)" if self.engine
+                else "oracle.run_static (restatement of traverse.py:235-260)")
+
+    def sweep(self, z0: int, z1: int, threads: int) -> float:
+        """Planes [z0, z1) of the box through run_static; wall seconds."""
+        n = self.n
         t0 = time.perf_counter()
-        self.oracle.run_static(work, 0, P, self.threads)
+        if self.engine is not None:
+            self.engine.run_static(self.engine.IndexSpace((0, 0, z0), (n, n, z1)), self.kernel, threads)
+        else:
+            self.oracle.run_static(
+                lambda a, b: self.oracle.d4_all(self.outs, self.u, self.g, (0, n, 0, n, a, b), self.k), z0, z1, threads)
         return time.perf_counter() - t0
 
-    def sample(self, seconds: float) -> dict:
-        done, el = 0, 0.0
+    def sample(self, seconds: float, threads: int, planes: int) -> dict:
+        n = self.n
+        done, el, z = 0, 0.0, 0
         while el < seconds:
-            el += self.slab()
-            done += self.planes
-        pts = done * self.n * self.n
-        return {"value": pts / el / 1e9, "unit": UNIT, "cores": self.threads, "kind": "port",
-                "sample": f"{done} z-planes of 256x256 (= {pts} updates, {done // self.planes} slabs of "
-                          f"{self.planes} planes) of config 2, oracle numpy expression trees over "
-                          f"{self.threads} threads, {el:.2f} s"}
+            z1 = min(n, z + planes)
+            el += self.sweep(z, z1, threads)
+            done += z1 - z
+            z = 0 if z1 >= n else z1
+        pts = done * n * n
+        return {"value": pts / el / 1e9, "unit": UNIT, "cores": threads,
+                "sample": f"{done} z-planes of 256x256 (= {pts} updates, run_static calls of {planes} planes) of "
+                          f"config 2 in {el:.2f} s"}
+
+
+def c1_reference_drivers(seconds: float = 3.0) -> dict | None:
+    """The reference's literal C1 drivers (stencil.py:55-94) at n = 66
+    (64^3 interior), from baseline/_ref: run_serial (1 thread), run_naive
+    (all threads), run_tuned (after 40 tuning iterations)."""
+    if reference_engine() is None:
+        return None
+    import stencilrt.stencil as st
+    import stencilrt.tuner as tu
+    from oracle.stencils import host_threads
+    n, pts = 66, 64 ** 3
+    thr = host_threads()
+    out = {"engine": "stencilrt (baseline/_ref)", "n": n, "interior_pts": pts}
+
+    def rate(secs):
+        return pts * len(secs) / sum(secs) / 1e9
+
+    iters = max(8, int(seconds / 0.006))
+    out["run_serial"] = {"value": rate(st.run_serial(n, iters, 20130715).iter_seconds), "unit": UNIT, "cores": 1,
+                         "iters": iters}
+    out["run_naive"] = {"value": rate(st.run_naive(n, iters, 20130715, thr).iter_seconds), "unit": UNIT,
+                        "cores": thr, "iters": iters}
+    topo = tu.TopologyConfig(n_coarse_threads=thr, n_fine_threads=1)
+    run, _ = st.run_tuned(n, 40 + iters, 20130715, topo)
+    out["run_tuned"] = {"value": rate(run.iter_seconds[40:]), "unit": UNIT, "cores": thr, "iters": iters,
+                        "tuning_iters_discarded": 40}
+    return out
 
 
 def run_reference(args) -> None:
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    cpu = CpuOracle()
+    cpu = CpuC2()
+    n = cpu.n
     for _ in range(args.warmup):
-        cpu.slab()
-    secs = [cpu.slab() for _ in range(args.steps)]
-    pts = cpu.planes * cpu.n * cpu.n
-    v = statistics.median([pts / s / 1e9 for s in secs])
+        cpu.sweep(0, n, cpu.threads)
+    secs = [cpu.sweep(0, n, cpu.threads) for _ in range(args.steps)]
+    ms = sum(secs) / len(secs) * 1e3
+    v = n ** 3 / (ms * 1e-3) / 1e9
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 256 ** 3 / (v * 1e9) * 1e3,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (seeded host generator, BASELINE.json config 2 shapes)",
-           "config": dict(WORKLOAD, parallelism=f"host threads x{cpu.threads}"),
-           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu.threads, "kind": "port",
-                            "sample": f"each step: one slab of {cpu.planes} z-planes of 256x256 of config 2 "
-                                      f"({pts} updates), oracle numpy expression trees, {cpu.threads} threads; "
-                                      f"value = median over {args.steps} steps; ms_per_step extrapolated to 256^3"},
+           "config": dict(WORKLOAD, parallelism=f"host threads x{cpu.threads}", input_sha256=cpu.sha),
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu.threads, "kind": "port", "cpu_model": cpu_model(),
+                            "engine": cpu.engine_name,
+                            "sample": f"each step: one whole 256^3 sweep (all ten outputs) through {cpu.engine_name} "
+                                      f"over {cpu.threads} threads, piece kernel = oracle numpy expression trees; "
+                                      f"value = total updates / total wall time of the {args.steps} timed steps",
+                            "step_seconds_median": statistics.median(secs)},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU side
+# ---------------------------------------------------------------------------
+
+def _timed_steps(step, steps: int, warmup: int, dev: int, stream) -> tuple[float, list[float], dict]:
+    """W untimed + K timed calls of step() on `stream`, CUDA events, clock
+    samples during the timed region; returns (total ms, per-step ms, clocks)."""
+    import torch
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    with ClockSampler(dev) as clk:
+        ev[0].record(stream)
+        for i in range(steps):
+            step()
+            ev[i + 1].record(stream)
+        clk.wait(ev[-1])
+        torch.cuda.synchronize()
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+    return ev[0].elapsed_time(ev[-1]), per, clk.summary()
+
+
+def extra_legs(args, dev: int, stream, hbm_peak: float) -> dict:
+    """Configs 1, 3, 4, 5 on this GPU, each timed like the main leg."""
+    import torch
+    from paper_1308_1343_b200 import inputs
+    from paper_1308_1343_b200.configs import C1Laplacian7, C3WaveRK4, C4Level, C5Rhs24
+    from paper_1308_1343_b200.graphs import SweepGraph
+    from paper_1308_1343_b200.grid import DeviceGrid
+    from paper_1308_1343_b200.kernels import Laplacian7
+    out = {}
+    K, W = args.steps, args.warmup
+
+    # C1: the 64^3 7-point sweep, L2-resident and launch-bound: a CUDA graph
+    # of 50 ping-pong sweep pairs (programmatic dependent launch between them)
+    p = C1Laplacian7().setup()
+    b = DeviceGrid((p.n,) * 3, 1)
+    b.upload(p.host_u, with_ghosts=True)
+    ka, kb = Laplacian7(b, p.src, p.c0, p.c1), Laplacian7(p.src, b, p.c0, p.c1)
+
+    def pair():
+        ka.launch(p.space, ka.default_params)
+        kb.launch(p.space, kb.default_params)
+    reps = 50
+    g = SweepGraph(pair, repeat=reps, warmup=1)
+    ms, per, clk = _timed_steps(g.replay, K, W, dev, stream)
+    sweep_ms = ms / (K * 2 * reps)
+    out["c1_lap7_64^3"] = {
+        "step": f"one CUDA-graph replay of {2 * reps} Jacobi sweeps (ping-pong); value per sweep",
+        "ms_per_sweep": sweep_ms, "value": p.updates / (sweep_ms * 1e-3) / 1e9, "unit": UNIT,
+        "bound": "launch / L2 (4.4 MB working set)", "algorithmic_bytes": p.canonical_bytes,
+        "achieved_gbs": p.canonical_bytes / (sweep_ms * 1e-3) / 1e9, "gpu_launches": K * 2 * reps,
+        "clocks": clk, "input_sha256": inputs.sha256(p.host_u)}
+    del p, b, g, ka, kb
+    torch.cuda.empty_cache()
+
+    # C3: one classical RK4 step of the 384^3 periodic wave problem
+    p = C3WaveRK4().setup()
+    ms, per, clk = _timed_steps(p.run, K, W, dev, stream)
+    step_ms = ms / K
+    ach = p.canonical_bytes / (step_ms * 1e-3) / 1e9
+    out["c3_wave_rk4_384^3"] = {
+        "step": "one RK4 step (two launches: Laplacian pairs with fused periodic ghost refresh)",
+        "ms_per_step": step_ms, "ms_per_step_median": statistics.median(per),
+        "value": p.updates / (step_ms * 1e-3) / 1e9, "unit": UNIT,
+        "roofline": {"bound": "issue / FP64 latency (ncu, profiles/README.md)", "achieved": ach, "peak": hbm_peak,
+                     "unit": "GB/s", "frac": ach / hbm_peak, "algorithmic_bytes_per_step": p.canonical_bytes,
+                     "bytes_rule": "10 array passes of the Laplacian-pair schedule + 6 ghost shells",
+                     "survey_34pass_bytes": p.survey_canonical_bytes,
+                     "survey_34pass_gbs": p.survey_canonical_bytes / (step_ms * 1e-3) / 1e9},
+        "gpu_launches": 2 * K, "clocks": clk,
+        "input_sha256": {"phi0": inputs.sha256(p.host_phi), "pi0": inputs.sha256(p.host_pi)}}
+    del p
+    torch.cuda.empty_cache()
+
+    # C4: 4th-order Laplacian of the 512^3-minus-octant level, 3 boxes, one launch
+    p = C4Level().setup()
+    ms, per, clk = _timed_steps(p.run, K, W, dev, stream)
+    step_ms = ms / K
+    ach = p.canonical_bytes / (step_ms * 1e-3) / 1e9
+    out["c4_level_lap4_512^3"] = {
+        "step": "one launch over all 3 boxes of the level", "ms_per_step": step_ms,
+        "ms_per_step_median": statistics.median(per), "value": p.updates / (step_ms * 1e-3) / 1e9, "unit": UNIT,
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                     "algorithmic_bytes_per_step": p.canonical_bytes},
+        "gpu_launches": K, "clocks": clk, "boxes": [[list(b.lo), list(b.hi)] for b in p.boxes],
+        "input_sha256": [inputs.sha256(u) for u in p.host_u]}
+    del p
+    torch.cuda.empty_cache()
+
+    # C5: the fused 24-variable right-hand side
+    p = C5Rhs24().setup()
+    ms, per, clk = _timed_steps(p.run, K, W, dev, stream)
+    step_ms = ms / K
+    fpk = fp64_peak()
+    ops = p.fp64_ops / (step_ms * 1e-3)
+    out["c5_rhs24_192^3"] = {
+        "step": "one fused sweep (24 inputs -> 24 outputs)", "ms_per_step": step_ms,
+        "ms_per_step_median": statistics.median(per), "value": p.updates / (step_ms * 1e-3) / 1e9, "unit": UNIT,
+        "roofline": {"bound": "fp64 (unfused DADD/DMUL)", "achieved": ops / 1e12, "unit": "T FP64 ops/s",
+                     "peak": fpk / 1e12 if fpk else None,
+                     "peak_source": "measured, profiles/r01/pipe_ceiling.json (tools/pipe_ceiling.py)",
+                     "frac": ops / fpk if fpk else None, "fp64_ops_per_step": p.fp64_ops,
+                     "hbm_gbs": p.canonical_bytes / (step_ms * 1e-3) / 1e9,
+                     "algorithmic_bytes_per_step": p.canonical_bytes},
+        "gpu_launches": K, "clocks": clk,
+        "input_sha256": inputs.sha256(np.stack(p.host_u)), "poly_sha256": inputs.sha256(p.poly.coef)}
+    del p
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_ours(args) -> None:
@@ -224,7 +426,7 @@ def run_ours(args) -> None:
         else:
             dist.init_process_group(backend)
 
-    from paper_1308_1343_b200 import _build
+    from paper_1308_1343_b200 import _build, inputs
     from paper_1308_1343_b200.configs import C2FourthOrder
     from paper_1308_1343_b200.tuner import LaunchParams
 
@@ -343,37 +545,56 @@ def run_ours(args) -> None:
     e2e_value = updates / (e2e_ms * 1e-3) / 1e9
     # results really came back: spot-check the host copy of Lap4 against the device
     ok = torch.equal(h_out[9][:2].cuda(), prob.outs[9].interior()[:2])
+    del h_in, h_out
+
+    h2d_bytes, d2h_bytes = prob.h2d_bytes, prob.d2h_bytes
+    peaks = measured_peaks()
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    extra = None
+    if not args.no_extra and world == 1:
+        del prob.outs, prob.kernel, prob.src
+        torch.cuda.empty_cache()
+        extra = extra_legs(args, dev, stream, peak)
 
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return
 
-    peaks = measured_peaks()
-    peak = float(peaks.get("hbm_gbs", 6650.0))
     kernel_ms = statistics.mean(per)
     achieved = prob.canonical_bytes / (kernel_ms * 1e-3) / 1e9
     traffic = ncu_traffic()
-    cpu = None if args.no_cpu or world > 1 else CpuOracle().sample(args.ref_seconds)
+    cpu = None
+    if not args.no_cpu and world == 1:
+        c2 = CpuC2()
+        cpu = c2.sample(args.ref_seconds, c2.threads, 32)
+        cpu.update({"kind": "port", "cpu_model": cpu_model(), "engine": c2.engine_name,
+                    "sample": cpu["sample"] + f", {c2.threads} threads, piece kernel = oracle numpy expression trees"})
+        one = c2.sample(args.ref_seconds_1t, 1, 4)
+        cpu["one_thread"] = dict(one, kind="port", engine=c2.engine_name)
+        cpu["c1_reference_drivers"] = c1_reference_drivers()
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded host generator, BASELINE.json config 2 shapes)",
-        "config": dict(WORKLOAD, parallelism=f"box-per-rank x{world}",
+        "config": dict(WORKLOAD, parallelism=f"box-per-rank x{world}", input_sha256=inputs.sha256(prob.host_u),
                        launch={"tile_x": params.tile_x, "tile_y": params.tile_y, "z_chunk": params.z_chunk,
                                "points_per_thread": params.points_per_thread}, tuning=tune_info),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks else "fallback",
+                     "traffic": traffic,
+                     "traffic_source": "ncu --set full, profiles/ncu_summary.json (builder capture, not this run)",
+                     "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks else "fallback",
                      "algorithmic_bytes_per_launch": prob.canonical_bytes, "kernel_ms_mean": kernel_ms,
                      "kernel_ms_median": statistics.median(per), "kernel": "d4_kernel<ALL10> (sb_d4_all)"},
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": prob.h2d_bytes,
-                "d2h_bytes_per_step": prob.d2h_bytes, "ms_per_step": e2e_ms, "steps": e2e_steps,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_bytes,
+                "d2h_bytes_per_step": d2h_bytes, "ms_per_step": e2e_ms, "steps": e2e_steps,
                 "results_checked": bool(ok)},
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
         "clocks_e2e": clk_e2e.summary(),
         "sustained": sustained,
+        "extra": extra,
     }
     print(json.dumps(out), flush=True)
     if dist:
@@ -392,8 +613,10 @@ def main(argv=None):
                     metavar=("TILE_X", "TILE_Y", "Z_CHUNK", "POINTS_PER_THREAD"))
     ap.add_argument("--tune", type=int, default=40, help="tuner executions during warm-up (0 = kernel default)")
     ap.add_argument("--e2e-steps", dest="e2e_steps", type=int, default=10)
-    ap.add_argument("--ref-seconds", dest="ref_seconds", type=float, default=12.0)
+    ap.add_argument("--ref-seconds", dest="ref_seconds", type=float, default=10.0)
+    ap.add_argument("--ref-seconds-1t", dest="ref_seconds_1t", type=float, default=5.0)
     ap.add_argument("--no-cpu", dest="no_cpu", action="store_true")
+    ap.add_argument("--no-extra", dest="no_extra", action="store_true", help="skip the config 1/3/4/5 legs")
     ap.add_argument("--sustained-steps", dest="sustained_steps", type=int, default=3000,
                     help="extra back-to-back steps timed after the main region (0 = skip)")
     args = ap.parse_args(argv)

@@ -197,6 +197,11 @@ class C5Rhs24:
         self.k = inputs.D4Constants.for_spacing(1.0 / n)
         self.updates = n ** 3
         self.canonical_bytes = 8 * inputs.N_VARS * (_vol((n,) * 3, g) + n ** 3)
+        # algorithmic unfused FP64 operations per step, with every reusable
+        # intermediate computed once: per variable and point rx, ry (4 each),
+        # Dx, Dy (1 each), Dz (5), Dxx, Dyy, Dzz (7 each), Dxy, Dxz, Dyz (5 each)
+        # = 51; per output 64 terms x 2 multiplies + 63 additions
+        self.fp64_ops = n ** 3 * (inputs.N_VARS * 51 + inputs.N_VARS * (3 * inputs.N_TERMS - 1))
 
     def setup(self, device=None):
         n = self.n
