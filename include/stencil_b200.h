@@ -59,7 +59,9 @@ extern "C" {
 #define SB_RESOURCE 2
 #define SB_CUDA 3
 
-#define SB_MAX_BOXES 8     /* boxes per batched launch (sb_lap4_boxes) */
+#define SB_MAX_BOXES 8     /* boxes whose table travels in the launch parameters; a
+                              launch over more boxes (any number) uses a device-resident
+                              box table the library builds once per level shape */
 #define SB_N_D4_OUT 10     /* Dx Dy Dz Dxx Dyy Dzz Dxy Dxz Dyz Lap4 */
 #define SB_N_VARS 24       /* config-5 grid functions */
 #define SB_N_TERMS 64      /* config-5 terms per output polynomial */
@@ -193,11 +195,32 @@ SB_API int sb_d4_all(const sb_array *out, sb_array src, sb_space space,
 SB_API int sb_d2_all(const sb_array *out, sb_array src, sb_space space,
                      sb_d4_constants k, sb_launch p, void *stream);
 
-/* K3 — 4th-order Laplacian over up to SB_MAX_BOXES boxes of a level in one
- * launch (config 4); the device box table replaces execute_plan's block
- * queue (traverse.py:162-209). */
+/* K3 — 4th-order Laplacian over every box of a level in ONE launch
+ * (config 4; the boxes of BBoxSet.to_bboxes(), bboxset.py:313-317 ->
+ * traverse.py:59-65).  The box table (blockIdx -> box by binary search on
+ * each box's first tile) replaces execute_plan's block queue
+ * (traverse.py:162-209).  Up to SB_MAX_BOXES boxes travel in the launch
+ * parameters; larger levels use a device-resident table that the first
+ * launch of a (box list, launch shape) builds and uploads — that first
+ * launch waits for the upload and is refused inside a CUDA-graph capture;
+ * later launches of the same shape are pure launches.  Tables are released
+ * by sb_release_tables. */
 SB_API int sb_lap4_boxes(const sb_box_job *jobs, int32_t njobs, sb_d4_constants k,
                   sb_launch p, void *stream);
+
+/* K2 over a level: all ten 4th-order (sb_d4_all_boxes) or 2nd-order
+ * (sb_d2_all_boxes) outputs of every box in one launch (same box table). */
+typedef struct sb_d4_all_job {
+    sb_array out[SB_N_D4_OUT];
+    sb_array src;
+    sb_space space;
+} sb_d4_all_job;
+
+SB_API int sb_d4_all_boxes(const sb_d4_all_job *jobs, int32_t njobs, sb_d4_constants k, sb_launch p, void *stream);
+SB_API int sb_d2_all_boxes(const sb_d4_all_job *jobs, int32_t njobs, sb_d4_constants k, sb_launch p, void *stream);
+
+/* Free the library's cached device box tables (waits for the device). */
+SB_API int sb_release_tables(void);
 
 /* K4 — periodic refill of the ghost shell of `a` (every ghost point becomes
  * the interior point at its periodic image). */
@@ -206,6 +229,17 @@ SB_API int sb_ghost_periodic(sb_array a, void *stream);
 /* K5 — one classical RK4 stage (1..4) of d/dt(phi, pi) = (pi, Lap4 phi). */
 SB_API int sb_rk4_stage(int32_t stage, const sb_rk4_fields *f, sb_space space,
                  sb_rk4_constants c, sb_launch p, void *stream);
+
+/* K5 over a level: one RK4 stage of every box in one launch (the boxes'
+ * phi_s ghosts filled beforehand, e.g. by sb_copy_regions; no periodic
+ * refresh: SB_LAUNCH_PERIODIC_GHOSTS is refused). */
+typedef struct sb_rk4_box_job {
+    sb_rk4_fields f;
+    sb_space space;
+} sb_rk4_box_job;
+
+SB_API int sb_rk4_stage_boxes(int32_t stage, const sb_rk4_box_job *jobs, int32_t njobs, sb_rk4_constants c,
+                              sb_launch p, void *stream);
 
 /* K5b — the same RK4 step as two fused launches (temporal blocking):
  * pair 1 = stages 1+2: reads phi0, pi0 (ghosts valid), writes phi_out = phi3,

@@ -210,12 +210,10 @@ int sb_lap7_iterate(sb_array a, sb_array b, sb_space space, double c0, double c1
 }
 
 namespace {
-int all10(int mode, const char *nm, const sb_array *out, sb_array src, sb_space space, sb_d4_constants k,
-          sb_launch p, void *stream) {
+int all10_job(const char *nm, const sb_array *out, const sb_array &src, const sb_space &space, D4Job &job) {
     int rc;
     if (!out) return fail(SB_USAGE, "all outputs: null output table");
     if ((rc = check_array(src, 2, nm)) || (rc = check_space(space, src, nm))) return rc;
-    D4Job job;
     memset(&job, 0, sizeof(job));
     job.src = src;
     job.space = space;
@@ -224,52 +222,29 @@ int all10(int mode, const char *nm, const sb_array *out, sb_array src, sb_space 
             return rc;
         job.g[i] = out[i];
     }
+    return SB_OK;
+}
+
+int all10(int mode, const char *nm, const sb_array *out, sb_array src, sb_space space, sb_d4_constants k,
+          sb_launch p, void *stream) {
+    D4Job job;
+    if (int rc = all10_job(nm, out, src, space, job)) return rc;
     return launch_d4(mode, &job, 1, k, 0.0, p, as_stream(stream));
 }
 
-}  // namespace
-
-int sb_d4_all(const sb_array *out, sb_array src, sb_space space, sb_d4_constants k, sb_launch p, void *stream) {
-    return all10(D4_ALL10, "d4_all", out, src, space, k, p, stream);
-}
-
-int sb_d2_all(const sb_array *out, sb_array src, sb_space space, sb_d4_constants k, sb_launch p, void *stream) {
-    return all10(D2_ALL10, "d2_all", out, src, space, k, p, stream);
-}
-
-int sb_lap4_boxes(const sb_box_job *jobs, int32_t njobs, sb_d4_constants k, sb_launch p, void *stream) {
+int all10_boxes(int mode, const char *nm, const sb_d4_all_job *jobs, int32_t njobs, sb_d4_constants k, sb_launch p,
+                void *stream) {
     if (njobs == 0) return SB_OK;
-    if (!jobs || njobs < 0) return fail(SB_USAGE, "lap4_boxes: bad job table");
-    if (njobs > SB_MAX_BOXES) return fail(SB_RESOURCE, "lap4_boxes: more than SB_MAX_BOXES boxes in one launch");
-    D4Job dj[SB_MAX_BOXES];
-    memset(dj, 0, sizeof(dj));
-    int rc;
-    for (int j = 0; j < njobs; ++j) {
-        if ((rc = check_array(jobs[j].src, 2, "lap4 src")) || (rc = check_array(jobs[j].dst, 0, "lap4 dst")))
-            return rc;
-        if ((rc = check_space(jobs[j].space, jobs[j].src, "lap4")) ||
-            (rc = check_space(jobs[j].space, jobs[j].dst, "lap4 dst")))
-            return rc;
-        dj[j].src = jobs[j].src;
-        dj[j].space = jobs[j].space;
-        dj[j].g[0] = jobs[j].dst;
-    }
-    return launch_d4(D4_LAP4, dj, njobs, k, 0.0, p, as_stream(stream));
+    if (!jobs || njobs < 0) return fail(SB_USAGE, "all outputs over boxes: bad job table");
+    std::vector<D4Job> dj(njobs);
+    for (int j = 0; j < njobs; ++j)
+        if (int rc = all10_job(nm, jobs[j].out, jobs[j].src, jobs[j].space, dj[j])) return rc;
+    return launch_d4(mode, dj.data(), njobs, k, 0.0, p, as_stream(stream));
 }
 
-int sb_ghost_periodic(sb_array a, void *stream) {
-    int rc = check_array(a, 0, "ghost_periodic");
-    if (rc) return rc;
-    return launch_ghost_periodic(a, as_stream(stream));
-}
-
-int sb_rk4_stage(int32_t stage, const sb_rk4_fields *f, sb_space space, sb_rk4_constants c, sb_launch p,
-                 void *stream) {
-    return sb_rk4_stage_zslab(stage, f, space, c, p, nullptr, stream);
-}
-
-int sb_rk4_stage_zslab(int32_t stage, const sb_rk4_fields *f, sb_space space, sb_rk4_constants c, sb_launch p,
-                       const sb_zslab *zs, void *stream) {
+// The D4Job of one RK4 stage (mode, the stage's pointwise coefficient).
+int rk_job(int32_t stage, const sb_rk4_fields *f, const sb_space &space, const sb_rk4_constants &c, D4Job &job,
+           int &mode, double &ca) {
     if (!f) return fail(SB_USAGE, "rk4_stage: null fields");
     if (stage < 1 || stage > 4) return fail(SB_USAGE, "rk4_stage: stage must be 1..4");
     int rc;
@@ -279,7 +254,6 @@ int sb_rk4_stage_zslab(int32_t stage, const sb_rk4_fields *f, sb_space space, sb
         if (stage == 1 && (a == &f->pi_s || a == &f->phi0)) continue;
         if ((rc = check_array(*a, 0, "rk4 field")) || (rc = check_space(space, *a, "rk4 field"))) return rc;
     }
-    D4Job job;
     memset(&job, 0, sizeof(job));
     job.src = f->phi_s;
     job.space = space;
@@ -287,8 +261,6 @@ int sb_rk4_stage_zslab(int32_t stage, const sb_rk4_fields *f, sb_space space, sb
     job.g[1] = f->pi_out;
     job.g[2] = f->acc_phi;
     job.g[3] = f->acc_pi;
-    int mode;
-    double ca;
     if (stage == 1) {
         job.g[4] = f->pi0;
         mode = D4_RK1;
@@ -309,6 +281,79 @@ int sb_rk4_stage_zslab(int32_t stage, const sb_rk4_fields *f, sb_space space, sb
         mode = stage == 4 ? D4_RK4 : D4_RK23;
         ca = stage == 3 ? c.dt : c.dt6;
     }
+    return SB_OK;
+}
+
+}  // namespace
+
+int sb_d4_all(const sb_array *out, sb_array src, sb_space space, sb_d4_constants k, sb_launch p, void *stream) {
+    return all10(D4_ALL10, "d4_all", out, src, space, k, p, stream);
+}
+
+int sb_d2_all(const sb_array *out, sb_array src, sb_space space, sb_d4_constants k, sb_launch p, void *stream) {
+    return all10(D2_ALL10, "d2_all", out, src, space, k, p, stream);
+}
+
+int sb_d4_all_boxes(const sb_d4_all_job *jobs, int32_t njobs, sb_d4_constants k, sb_launch p, void *stream) {
+    return all10_boxes(D4_ALL10, "d4_all_boxes", jobs, njobs, k, p, stream);
+}
+
+int sb_d2_all_boxes(const sb_d4_all_job *jobs, int32_t njobs, sb_d4_constants k, sb_launch p, void *stream) {
+    return all10_boxes(D2_ALL10, "d2_all_boxes", jobs, njobs, k, p, stream);
+}
+
+int sb_lap4_boxes(const sb_box_job *jobs, int32_t njobs, sb_d4_constants k, sb_launch p, void *stream) {
+    if (njobs == 0) return SB_OK;
+    if (!jobs || njobs < 0) return fail(SB_USAGE, "lap4_boxes: bad job table");
+    std::vector<D4Job> dj(njobs);
+    int rc;
+    for (int j = 0; j < njobs; ++j) {
+        if ((rc = check_array(jobs[j].src, 2, "lap4 src")) || (rc = check_array(jobs[j].dst, 0, "lap4 dst")))
+            return rc;
+        if ((rc = check_space(jobs[j].space, jobs[j].src, "lap4")) ||
+            (rc = check_space(jobs[j].space, jobs[j].dst, "lap4 dst")))
+            return rc;
+        memset(&dj[j], 0, sizeof(D4Job));
+        dj[j].src = jobs[j].src;
+        dj[j].space = jobs[j].space;
+        dj[j].g[0] = jobs[j].dst;
+    }
+    return launch_d4(D4_LAP4, dj.data(), njobs, k, 0.0, p, as_stream(stream));
+}
+
+int sb_rk4_stage_boxes(int32_t stage, const sb_rk4_box_job *jobs, int32_t njobs, sb_rk4_constants c, sb_launch p,
+                       void *stream) {
+    if (njobs == 0) return SB_OK;
+    if (!jobs || njobs < 0) return fail(SB_USAGE, "rk4_stage_boxes: bad job table");
+    if (p.flags & SB_LAUNCH_PERIODIC_GHOSTS)
+        return fail(SB_USAGE, "rk4_stage_boxes: the periodic ghost refresh is for one periodic box (sb_rk4_stage)");
+    std::vector<D4Job> dj(njobs);
+    int mode = 0;
+    double ca = 0;
+    for (int j = 0; j < njobs; ++j)
+        if (int rc = rk_job(stage, &jobs[j].f, jobs[j].space, c, dj[j], mode, ca)) return rc;
+    return launch_d4(mode, dj.data(), njobs, c.lap, ca, p, as_stream(stream));
+}
+
+int sb_release_tables(void) { return release_box_tables(); }
+
+int sb_ghost_periodic(sb_array a, void *stream) {
+    int rc = check_array(a, 0, "ghost_periodic");
+    if (rc) return rc;
+    return launch_ghost_periodic(a, as_stream(stream));
+}
+
+int sb_rk4_stage(int32_t stage, const sb_rk4_fields *f, sb_space space, sb_rk4_constants c, sb_launch p,
+                 void *stream) {
+    return sb_rk4_stage_zslab(stage, f, space, c, p, nullptr, stream);
+}
+
+int sb_rk4_stage_zslab(int32_t stage, const sb_rk4_fields *f, sb_space space, sb_rk4_constants c, sb_launch p,
+                       const sb_zslab *zs, void *stream) {
+    D4Job job;
+    int mode = 0;
+    double ca = 0;
+    if (int rc = rk_job(stage, f, space, c, job, mode, ca)) return rc;
     if (zs && ((zs->lo_phi_out && !aligned16(zs->lo_phi_out)) || (zs->hi_phi_out && !aligned16(zs->hi_phi_out))))
         return fail(SB_USAGE, "rk4_stage_zslab: peer origins must be 16-byte aligned");
     return launch_d4(mode, &job, 1, c.lap, ca, p, as_stream(stream), zs);

@@ -111,6 +111,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     if (__builtin_expect(!mbar_try(bar, parity), 0)) mbar_wait_slow(bar, parity);
 }
 
+// A tensor map that lives in global memory and was written through the
+// generic proxy (a host copy into a library-owned table): order that write
+// before the TMA unit reads the descriptor (and drop any stale copy the
+// tensor-map cache holds for a reused address).
+__device__ __forceinline__ void tensormap_acquire(const CUtensorMap *m) {
+    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(reinterpret_cast<uint64_t>(m))
+                 : "memory");
+}
+
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *m) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }

@@ -29,6 +29,11 @@
 //   D_ab = d1u_a(d1u_b)*k11 with b the inner (x for xy/xz, y for yz) axis,
 //   Lap4 = (Dxx + Dyy) + Dzz.
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.h"
@@ -80,7 +85,8 @@ __host__ __device__ constexpr int lb_minb(int mode, int tyc) {
     return tyc > 0 && mode == D4_LAP4 ? SB_D4_LAP4_MINB_T : min_blocks(mode);
 }
 
-struct BoxDesc {
+// One box of the launch's box table.
+struct alignas(64) BoxDesc {
     CUtensorMap tmap;          // plane boxes of (TX+4) x (TY+4) x 1 over the source grid
     double *g[10];             // mode-dependent outputs / pointwise inputs (origins)
     long long sy, sz;          // strides shared by every g[] of the box
@@ -91,12 +97,25 @@ struct BoxDesc {
     int tile_begin;
 };
 
+// RK stages: TMA maps of a box's pointwise operands (TX x TY x 1 boxes at
+// interior coordinates), staged next to the stencil plane.
+struct alignas(64) PwDesc {
+    CUtensorMap map[5];
+    int tma0[5][3];
+};
+
+constexpr int kInlineBoxes = 8;
+
 struct D4Params {
-    BoxDesc box[SB_MAX_BOXES];
-    // RK stages (single box): TMA maps of the pointwise operands (TX x TY x 1
-    // boxes at interior coordinates), staged next to the stencil plane
-    CUtensorMap pwmap[5];
-    int pw_tma0[5][3];
+    // Box table: up to kInlineBoxes boxes travel in the parameters; larger
+    // levels (and RK stages over several boxes) use a device-resident table
+    // (gbox / gpw / gbegin, built once per level shape and cached by the
+    // library, box_table() below) searched by binary search on tile_begin.
+    BoxDesc box[kInlineBoxes];
+    PwDesc pw0;                // pointwise maps of box 0 (inline table)
+    const BoxDesc *gbox;       // device table, or null
+    const PwDesc *gpw;         // device pointwise maps (RK modes), or null
+    const int *gbegin;         // device tile_begin[nbox]
     int per[3];                // periodic extents for fused ghost stores (0 = none)
     int pghost;                // ghost width refreshed by the fused stores
     double *zlo, *zhi;         // z targets of points near the low / high face
@@ -129,7 +148,7 @@ struct Ctx {
 // (with halo) and, for the RK stages once outputs start (j >= 4), the
 // pointwise operand planes of output plane Z0-4+j.
 template <int MODE, int TX>
-__device__ __forceinline__ void issue_plane(const Ctx &c, const D4Params &P, const BoxDesc &B, int j, int s) {
+__device__ __forceinline__ void issue_plane(const Ctx &c, const PwDesc &PW, const BoxDesc &B, int j, int s) {
     constexpr int NPW = n_pointwise(MODE);
     double *st = const_cast<double *>(c.stages) + s * c.stage_elems;
     const bool with_pw = NPW > 0 && j >= 4;
@@ -145,8 +164,8 @@ __device__ __forceinline__ void issue_plane(const Ctx &c, const D4Params &P, con
             const int zc = c.Z0 - 4 + j;
 #pragma unroll
             for (int a = 0; a < NPW; ++a)
-                tma_load_3d(st + c.plane_elems + a * c.pw_elems, &P.pwmap[a], P.pw_tma0[a][0] + c.X0,
-                            P.pw_tma0[a][1] + c.Y0, P.pw_tma0[a][2] + zc, &c.full[s]);
+                tma_load_3d(st + c.plane_elems + a * c.pw_elems, &PW.map[a], PW.tma0[a][0] + c.X0,
+                            PW.tma0[a][1] + c.Y0, PW.tma0[a][2] + zc, &c.full[s]);
         }
     }
 }
@@ -165,7 +184,7 @@ __device__ __forceinline__ void store_periodic(double *base, long long sy, long 
 
 template <int MODE, int TX, int NP, int R>
 __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &P, const BoxDesc &B,
-                                           const Lanes<NP> &L, Rings<NP> &rg) {
+                                           const PwDesc &PW, const Lanes<NP> &L, Rings<NP> &rg) {
     constexpr int W = TX + 4;
     if (i >= c.nplanes) return true;
     const int s = i & (kStages - 1);
@@ -234,7 +253,7 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
 
     // every thread is done with stage s (and rx of this plane is visible)
     named_bar(1, c.nthr);
-    if (c.tid == 0 && i + kStages < c.nplanes) issue_plane<MODE, TX>(c, P, B, i + kStages, s);
+    if (c.tid == 0 && i + kStages < c.nplanes) issue_plane<MODE, TX>(c, PW, B, i + kStages, s);
 
     if constexpr (all10(MODE)) {
         if (z >= c.Z0 && z < c.Z1) {
@@ -346,7 +365,10 @@ __device__ __forceinline__ bool plane_step(int i, const Ctx &c, const D4Params &
 
 // TYC > 0: compile-time tile height (the default shapes), so staged-plane
 // offsets fold into immediates; TYC = 0: P.ty
-template <int MODE, int TX, int NP, int TYC>
+// GT: the box table is device-resident (P.gbox / P.gpw / P.gbegin) instead
+// of inline in the parameters (whose fields the compiler reads as
+// constant-bank operands, keeping them out of registers).
+template <int MODE, int TX, int NP, int TYC, bool GT>
 __global__ void __launch_bounds__(lb_threads(MODE, TX, NP, TYC), lb_minb(MODE, TYC))
     d4_kernel(const __grid_constant__ D4Params P) {
     pdl_launch_dependents();    // PDL: see lap7.cu
@@ -369,10 +391,19 @@ __global__ void __launch_bounds__(lb_threads(MODE, TX, NP, TYC), lb_minb(MODE, T
     // ---- box table lookup: blockIdx.x -> (box, tile) ----
     int t = blockIdx.x;
     int b = 0;
-    if constexpr (MODE == D4_LAP4) {
+    if constexpr (GT) {        // device table: binary search on tile_begin
+        int lo = 0, hi = P.nbox - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (t >= __ldg(P.gbegin + mid)) lo = mid;
+            else hi = mid - 1;
+        }
+        b = lo;
+    } else {
         while (b + 1 < P.nbox && t >= P.box[b + 1].tile_begin) ++b;
     }
-    const BoxDesc &B = P.box[b];
+    const BoxDesc &B = GT ? P.gbox[b] : P.box[b];
+    const PwDesc &PW = GT && n_pointwise(MODE) > 0 ? P.gpw[b] : P.pw0;
     t -= B.tile_begin;
     const int bx = t % B.ntx;
     t /= B.ntx;
@@ -403,8 +434,13 @@ __global__ void __launch_bounds__(lb_threads(MODE, TX, NP, TYC), lb_minb(MODE, T
     if (c.tid == 0) {
         for (int s = 0; s < kStages; ++s) mbar_init(&c.full[s], 1);
         fence_mbar_init();
+        if constexpr (GT) {    // descriptors written through the generic proxy (host copy)
+            tensormap_acquire(&B.tmap);
+            if constexpr (n_pointwise(MODE) > 0)
+                for (int a = 0; a < n_pointwise(MODE); ++a) tensormap_acquire(&PW.map[a]);
+        }
         tma_prefetch_desc(&B.tmap);
-        for (int i = 0; i < kStages && i < c.nplanes; ++i) issue_plane<MODE, TX>(c, P, B, i, i);
+        for (int i = 0; i < kStages && i < c.nplanes; ++i) issue_plane<MODE, TX>(c, PW, B, i, i);
     }
     __syncthreads();
 
@@ -415,11 +451,11 @@ __global__ void __launch_bounds__(lb_threads(MODE, TX, NP, TYC), lb_minb(MODE, T
         for (int j = 0; j < NP; ++j) rg.u[k][j] = rg.s[k][j] = rg.rx[k][j] = rg.ry[k][j] = 0.0;
 
     for (int i = 0;; i += 5) {
-        if (plane_step<MODE, TX, NP, 0>(i + 0, c, P, B, L, rg)) break;
-        if (plane_step<MODE, TX, NP, 1>(i + 1, c, P, B, L, rg)) break;
-        if (plane_step<MODE, TX, NP, 2>(i + 2, c, P, B, L, rg)) break;
-        if (plane_step<MODE, TX, NP, 3>(i + 3, c, P, B, L, rg)) break;
-        if (plane_step<MODE, TX, NP, 4>(i + 4, c, P, B, L, rg)) break;
+        if (plane_step<MODE, TX, NP, 0>(i + 0, c, P, B, PW, L, rg)) break;
+        if (plane_step<MODE, TX, NP, 1>(i + 1, c, P, B, PW, L, rg)) break;
+        if (plane_step<MODE, TX, NP, 2>(i + 2, c, P, B, PW, L, rg)) break;
+        if (plane_step<MODE, TX, NP, 3>(i + 3, c, P, B, PW, L, rg)) break;
+        if (plane_step<MODE, TX, NP, 4>(i + 4, c, P, B, PW, L, rg)) break;
     }
 }
 
@@ -431,13 +467,19 @@ size_t smem_bytes(int mode, int tx, int ty) {
     return smem;
 }
 
-template <int MODE, int TX, int NP, int TYC>
-int launch_mode_ty(const D4Params &P, int nblocks, cudaStream_t st) {
+template <int MODE, int TX, int NP, int TYC, bool GT>
+int launch_mode_gt(const D4Params &P, int nblocks, cudaStream_t st) {
     const int threads = (TX / NP) * P.ty;
     const size_t smem = smem_bytes(MODE, TX, P.ty);
-    auto fn = d4_kernel<MODE, TX, NP, TYC>;
+    auto fn = d4_kernel<MODE, TX, NP, TYC, GT>;
     if (int rc = ensure_smem_limit((const void *)fn, 227 * 1024, "cudaFuncSetAttribute(d4)")) return rc;
     return launch_pdl(fn, dim3(nblocks), dim3(threads), smem, st, "d4_kernel launch", P);
+}
+
+template <int MODE, int TX, int NP, int TYC>
+int launch_mode_ty(const D4Params &P, int nblocks, cudaStream_t st) {
+    if (P.gbox) return launch_mode_gt<MODE, TX, NP, TYC, true>(P, nblocks, st);
+    return launch_mode_gt<MODE, TX, NP, TYC, false>(P, nblocks, st);
 }
 
 template <int MODE, int TX, int NP>
@@ -466,11 +508,149 @@ int launch_np(const D4Params &P, int tx, int np, int nblocks, cudaStream_t st) {
 
 bool same_strides(const sb_array &a, const sb_array &b) { return a.sy == b.sy && a.sz == b.sz; }
 
+bool empty_space(const sb_space &sp) {
+    bool e = false;
+    for (int d = 0; d < 3; ++d) e |= sp.hi[d] <= sp.lo[d];
+    return e;
+}
+
+int n_used(int mode) { return all10(mode) ? 10 : mode == D4_LAP4 ? 1 : mode == D4_RK1 ? 5 : mode == D4_RK2 ? 8 : 9; }
+
+// Fill one box-table entry; advances `total` (tiles before the next box).
+int fill_box(BoxDesc &D, const D4Job &J, int TX, int TY, int ZC, long long &total) {
+    const sb_space &sp = J.space;
+    if (int rc = make_tmap(&D.tmap, J.src, TX + 4, TY + 4, 1)) return rc;
+    for (int a = 0; a < 10; ++a) D.g[a] = J.g[a].origin;
+    D.sy = J.g[0].sy;
+    D.sz = J.g[0].sz;
+    D.tma0[0] = J.src.xpad;
+    D.tma0[1] = J.src.ghost;
+    D.tma0[2] = J.src.ghost;
+    for (int d = 0; d < 3; ++d) {
+        D.lo[d] = sp.lo[d];
+        D.hi[d] = sp.hi[d];
+    }
+    D.ax0 = (sp.lo[0] >= 0 ? sp.lo[0] / TX : -((-sp.lo[0] + TX - 1) / TX)) * TX;
+    D.ntx = (sp.hi[0] - D.ax0 + TX - 1) / TX;
+    D.nty = (sp.hi[1] - sp.lo[1] + TY - 1) / TY;
+    const int ntz = (sp.hi[2] - sp.lo[2] + ZC - 1) / ZC;
+    D.tile_begin = (int)total;
+    total += (long long)D.ntx * D.nty * ntz;
+    if (total > 0x7fffffffLL) return fail(SB_RESOURCE, "too many tiles for one launch");
+    return SB_OK;
+}
+
+int fill_pw(PwDesc &W, const D4Job &J, int npw, int TX, int TY) {
+    for (int a = 0; a < npw; ++a) {
+        const sb_array &A = J.g[4 + a];
+        if (int rc = make_tmap(&W.map[a], A, TX, TY, 1)) return rc;
+        W.tma0[a][0] = A.xpad;
+        W.tma0[a][1] = A.ghost;
+        W.tma0[a][2] = A.ghost;
+    }
+    return SB_OK;
+}
+
+// ---- device-resident box tables ------------------------------------------
+// Built on the first launch of a (mode, launch shape, box list) and cached
+// per device: [BoxDesc x n][PwDesc x n (RK modes)][int tile_begin x n].  The
+// key is the launch's geometry (array origins, strides, extents, spaces), so
+// a level swept again with the same shape reuses its table; tables are
+// released by sb_release_tables.  The first launch of a shape uploads the
+// table and waits for the copy (refused inside a CUDA-graph capture).
+struct DevTable {
+    void *buf = nullptr;
+    long long total = 0;
+};
+std::mutex g_tab_mu;
+std::map<std::pair<int, std::string>, DevTable> g_tables;
+
+void put(std::string &k, const void *p, size_t n) { k.append(static_cast<const char *>(p), n); }
+void put_array(std::string &k, const sb_array &a) {
+    put(k, &a.origin, sizeof a.origin);
+    put(k, &a.sy, sizeof a.sy);
+    put(k, &a.sz, sizeof a.sz);
+    const int32_t v[5] = {a.nx, a.ny, a.nz, a.ghost, a.xpad};
+    put(k, v, sizeof v);
+}
+
+int box_table(int mode, const D4Job *jobs, const std::vector<int> &live, int TX, int TY, int ZC, int NP,
+              cudaStream_t st, D4Params &P, long long &total_out) {
+    const int npw = n_pointwise(mode), nb = (int)live.size(), nused = n_used(mode);
+    int dev = 0;
+    if (int rc = check_cuda(cudaGetDevice(&dev), "cudaGetDevice")) return rc;
+    std::string key;
+    const int32_t hdr[5] = {mode, TX, TY, ZC, NP};
+    put(key, hdr, sizeof hdr);
+    for (int j : live) {
+        put_array(key, jobs[j].src);
+        put(key, jobs[j].space.lo, sizeof jobs[j].space.lo);
+        put(key, jobs[j].space.hi, sizeof jobs[j].space.hi);
+        for (int a = 0; a < nused; ++a) put_array(key, jobs[j].g[a]);
+    }
+    const size_t box_bytes = sizeof(BoxDesc) * nb, pw_bytes = npw ? sizeof(PwDesc) * nb : 0;
+    std::lock_guard<std::mutex> lock(g_tab_mu);
+    auto it = g_tables.find({dev, key});
+    if (it == g_tables.end()) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+            return fail(SB_USAGE, "box table: first launch of this level shape inside a CUDA-graph capture "
+                                  "(launch it once before capturing)");
+        std::vector<BoxDesc> boxes(nb);
+        std::vector<PwDesc> pws(npw ? nb : 0);
+        std::vector<int> begin(nb);
+        long long total = 0;
+        for (int i = 0; i < nb; ++i) {
+            if (int rc = fill_box(boxes[i], jobs[live[i]], TX, TY, ZC, total)) return rc;
+            begin[i] = boxes[i].tile_begin;
+            if (npw)
+                if (int rc = fill_pw(pws[i], jobs[live[i]], npw, TX, TY)) return rc;
+        }
+        std::vector<unsigned char> host(box_bytes + pw_bytes + sizeof(int) * nb);
+        memcpy(host.data(), boxes.data(), box_bytes);
+        if (npw) memcpy(host.data() + box_bytes, pws.data(), pw_bytes);
+        memcpy(host.data() + box_bytes + pw_bytes, begin.data(), sizeof(int) * nb);
+        DevTable t;
+        if (int rc = check_cuda(cudaMalloc(&t.buf, host.size()), "box table allocation")) return rc;
+        int rc = check_cuda(cudaMemcpyAsync(t.buf, host.data(), host.size(), cudaMemcpyHostToDevice, st),
+                            "box table upload");
+        if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "box table upload (wait)");
+        if (rc) {
+            cudaFree(t.buf);
+            return rc;
+        }
+        t.total = total;
+        it = g_tables.emplace(std::make_pair(dev, std::move(key)), t).first;
+    }
+    unsigned char *b = static_cast<unsigned char *>(it->second.buf);
+    P.gbox = reinterpret_cast<const BoxDesc *>(b);
+    P.gpw = npw ? reinterpret_cast<const PwDesc *>(b + box_bytes) : nullptr;
+    P.gbegin = reinterpret_cast<const int *>(b + box_bytes + pw_bytes);
+    P.nbox = nb;
+    total_out = it->second.total;
+    return SB_OK;
+}
+
 }  // namespace
+
+int release_box_tables() {
+    std::lock_guard<std::mutex> lock(g_tab_mu);
+    if (g_tables.empty()) return SB_OK;
+    int rc = check_cuda(cudaDeviceSynchronize(), "release box tables (wait)");
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto &kv : g_tables) {
+        cudaSetDevice(kv.first.first);
+        cudaFree(kv.second.buf);
+    }
+    cudaSetDevice(cur);
+    g_tables.clear();
+    return rc;
+}
 
 int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, double ca, const sb_launch &p,
               cudaStream_t st, const sb_zslab *zslab) {
-    if (njobs < 1 || njobs > SB_MAX_BOXES) return fail(SB_RESOURCE, "box count outside 1..SB_MAX_BOXES");
+    if (njobs < 0 || (njobs > 0 && !jobs)) return fail(SB_USAGE, "bad box job table");
     const int TX = p.tile_x, TY = p.tile_y, ZC = p.z_chunk;
     const int NP = (p.flags & SB_LAUNCH_SCALAR) ? 1 : 2;
     if (TX != 32 && TX != 64 && TX != 128) return fail(SB_USAGE, "tile_x must be 32, 64 or 128");
@@ -481,7 +661,20 @@ int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, 
                               "within the mode's limit (256 for paired d4_all / RK stages, else 512)");
     if (TY + 4 > 256) return fail(SB_USAGE, "tile_y + 4 exceeds the TMA box limit of 256");
     if (smem_bytes(mode, TX, TY) > 227 * 1024) return fail(SB_RESOURCE, "tile needs more than 227 KB of shared memory");
-    const int nused = all10(mode) ? 10 : mode == D4_LAP4 ? 1 : mode == D4_RK1 ? 5 : mode == D4_RK2 ? 8 : 9;
+    const int nused = n_used(mode), npw = n_pointwise(mode);
+
+    std::vector<int> live;
+    for (int j = 0; j < njobs; ++j) {
+        if (empty_space(jobs[j].space)) continue;
+        for (int a = 1; a < nused; ++a)
+            if (!same_strides(jobs[j].g[a], jobs[j].g[0]))
+                return fail(SB_USAGE, "all output / pointwise grids of one box must share row and plane strides");
+        live.push_back(j);
+    }
+    if (live.empty()) return SB_OK;
+    const bool periodic = npw > 0 && (p.flags & SB_LAUNCH_PERIODIC_GHOSTS);
+    if ((periodic || zslab) && live.size() != 1)
+        return fail(SB_USAGE, "periodic ghost refresh / z-slab halo stores sweep exactly one box");
 
     D4Params P;
     memset(&P, 0, sizeof(P));
@@ -492,55 +685,21 @@ int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, 
     P.k11 = k.k11;
     P.ca = ca;
     long long total = 0;
-    int nbox = 0;
-    for (int j = 0; j < njobs; ++j) {
-        const D4Job &J = jobs[j];
-        const sb_space &sp = J.space;
-        bool empty = false;
-        for (int d = 0; d < 3; ++d) empty |= sp.hi[d] <= sp.lo[d];
-        if (empty) continue;
-        for (int a = 1; a < nused; ++a)
-            if (!same_strides(J.g[a], J.g[0]))
-                return fail(SB_USAGE, "all output / pointwise grids of one box must share row and plane strides");
-        BoxDesc &D = P.box[nbox];
-        int rc = make_tmap(&D.tmap, J.src, TX + 4, TY + 4, 1);
-        if (rc) return rc;
-        for (int a = 0; a < 10; ++a) D.g[a] = J.g[a].origin;
-        D.sy = J.g[0].sy;
-        D.sz = J.g[0].sz;
-        D.tma0[0] = J.src.xpad;
-        D.tma0[1] = J.src.ghost;
-        D.tma0[2] = J.src.ghost;
-        for (int d = 0; d < 3; ++d) {
-            D.lo[d] = sp.lo[d];
-            D.hi[d] = sp.hi[d];
-        }
-        D.ax0 = (sp.lo[0] >= 0 ? sp.lo[0] / TX : -((-sp.lo[0] + TX - 1) / TX)) * TX;
-        D.ntx = (sp.hi[0] - D.ax0 + TX - 1) / TX;
-        D.nty = (sp.hi[1] - sp.lo[1] + TY - 1) / TY;
-        const int ntz = (sp.hi[2] - sp.lo[2] + ZC - 1) / ZC;
-        D.tile_begin = (int)total;
-        total += (long long)D.ntx * D.nty * ntz;
-        if (total > 0x7fffffffLL) return fail(SB_RESOURCE, "too many tiles for one launch");
-        ++nbox;
+    if (live.size() <= (size_t)kInlineBoxes && (npw == 0 || live.size() == 1)) {
+        for (size_t i = 0; i < live.size(); ++i)
+            if (int rc = fill_box(P.box[i], jobs[live[i]], TX, TY, ZC, total)) return rc;
+        if (npw)
+            if (int rc = fill_pw(P.pw0, jobs[live[0]], npw, TX, TY)) return rc;
+        P.nbox = (int)live.size();
+    } else {
+        if (int rc = box_table(mode, jobs, live, TX, TY, ZC, NP, st, P, total)) return rc;
     }
-    if (nbox == 0) return SB_OK;
-    if (nbox > 1 && mode != D4_LAP4) return fail(SB_USAGE, "only the Laplacian sweeps several boxes per launch");
-    P.nbox = nbox;
-    const int npw = n_pointwise(mode);
-    for (int a = 0; a < npw; ++a) {
-        const sb_array &A = jobs[0].g[4 + a];
-        int rc = make_tmap(&P.pwmap[a], A, TX, TY, 1);
-        if (rc) return rc;
-        P.pw_tma0[a][0] = A.xpad;
-        P.pw_tma0[a][1] = A.ghost;
-        P.pw_tma0[a][2] = A.ghost;
-    }
-    if (npw > 0 && (p.flags & SB_LAUNCH_PERIODIC_GHOSTS)) {
-        const sb_array &O = jobs[0].g[0];
+    const D4Job &J0 = jobs[live[0]];
+    if (periodic) {
+        const sb_array &O = J0.g[0];
         if (O.ghost < 1 || O.ghost > O.nx || O.ghost > O.ny || O.ghost > O.nz)
             return fail(SB_USAGE, "periodic ghost refresh needs 1 <= ghost <= every extent of phi_out");
-        const sb_space &sp = jobs[0].space;
+        const sb_space &sp = J0.space;
         for (int d = 0; d < 3; ++d)
             if (sp.lo[d] != 0 || sp.hi[d] != (d == 0 ? O.nx : d == 1 ? O.ny : O.nz))
                 return fail(SB_USAGE, "periodic ghost refresh needs the stage to sweep the whole interior");
@@ -561,6 +720,7 @@ int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, 
     } else if (zslab) {
         return fail(SB_USAGE, "z-slab halo stores need SB_LAUNCH_PERIODIC_GHOSTS");
     }
+    if (total == 0) return SB_OK;
     const int nb = (int)total;
     switch (mode) {
         case D4_ALL10: return launch_np<D4_ALL10>(P, TX, NP, nb, st);

@@ -73,6 +73,9 @@ struct D4Job {
 int launch_d4(int mode, const D4Job *jobs, int njobs, const sb_d4_constants &k, double ca, const sb_launch &p,
               cudaStream_t st, const sb_zslab *zslab = nullptr);
 
+// Free the device-resident box tables launch_d4 caches (sb_release_tables).
+int release_box_tables();
+
 int launch_ghost_periodic(const sb_array &a, cudaStream_t st);
 
 int launch_rk4_pair(int pair, const sb_array *halo, int nh, const sb_array *tile, int nt, const sb_array *out, int no,

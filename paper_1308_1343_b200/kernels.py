@@ -197,11 +197,55 @@ class Laplacian4(DeviceKernel):
                   _lib.launch_of(params, self.extra_flags), stream_ptr(stream))
 
 
-class LevelLaplacian4(DeviceKernel):
-    """K3 over a whole refinement level: every box in ONE launch through the
-    device box table (blockIdx -> (box, tile)).  ``launch`` ignores the space
-    argument's extent and sweeps each box's interior; ``__call__(piece)``
-    sweeps the part of ``piece`` inside each box (level coordinates)."""
+def _clip(box: IndexSpace, space) -> IndexSpace | None:
+    lo = tuple(max(a, b) for a, b in zip(box.lo, space.lo))
+    hi = tuple(min(a, b) for a, b in zip(box.hi, space.hi))
+    return None if any(h <= l for l, h in zip(lo, hi)) else IndexSpace(lo, hi)
+
+
+class _LevelKernel(DeviceKernel):
+    """A kernel over every box of a refinement level in ONE launch through
+    the device box table (blockIdx -> (box, tile); up to SB_MAX_BOXES boxes
+    travel in the launch parameters, larger levels use a table the library
+    builds on the first launch of a shape and caches).  ``launch`` sweeps each
+    box's interior (clipped to ``space`` when one is given, level
+    coordinates); ``__call__(piece)`` sweeps the part of ``piece`` inside
+    each box — so the reference's execute_plan/run_static can drive it."""
+
+    def _boxes(self):
+        raise NotImplementedError
+
+    def _job(self, i: int, space: IndexSpace):
+        raise NotImplementedError
+
+    def full_space(self) -> IndexSpace:
+        grids = [b[0] for b in self._boxes()]
+        lo = tuple(min(g.lower[d] for g in grids) for d in range(3))
+        hi = tuple(max(g.lower[d] + g.extents[d] for g in grids) for d in range(3))
+        return IndexSpace(lo, hi)
+
+    def _jobs(self, space):
+        jobs = []
+        for i, (grid, _) in enumerate(self._boxes()):
+            box = _interior_space(grid)
+            if space is not None:
+                box = _clip(box, space)
+                if box is None:
+                    continue
+            jobs.append(self._job(i, box))
+        return jobs
+
+    def launch(self, space: IndexSpace | None, params: LaunchParams, stream=None) -> None:
+        jobs = self._jobs(space)
+        if jobs:
+            self._run(jobs, params, stream)
+
+    def __call__(self, piece: IndexSpace) -> None:
+        self.launch(piece, self.default_params)
+
+
+class LevelLaplacian4(_LevelKernel):
+    """K3 over a whole refinement level (config 4): every box in ONE launch."""
 
     site_id = "lap4_level"
     space_kind = D4_SPACE
@@ -216,36 +260,88 @@ class LevelLaplacian4(DeviceKernel):
                 raise UsageError("4th-order stencils need ghost width >= 2")
         self.dsts, self.srcs, self.k = list(dsts), list(srcs), k
 
-    def full_space(self) -> IndexSpace:
-        lo = tuple(min(s.lower[d] for s in self.srcs) for d in range(3))
-        hi = tuple(max(s.lower[d] + s.extents[d] for s in self.srcs) for d in range(3))
-        return IndexSpace(lo, hi)
+    def _boxes(self):
+        return [(s, d) for s, d in zip(self.srcs, self.dsts)]
 
-    def _jobs(self, space: IndexSpace | None):
-        jobs = []
-        for d, s in zip(self.dsts, self.srcs):
-            box = _interior_space(s)
-            if space is not None:
-                lo = tuple(max(a, b) for a, b in zip(box.lo, space.lo))
-                hi = tuple(min(a, b) for a, b in zip(box.hi, space.hi))
-                if any(h <= l for l, h in zip(lo, hi)):
-                    continue
-                box = IndexSpace(lo, hi)
-            jobs.append(_lib.sb_box_job(d.abi(), s.abi(), _local(box, s)))
-        return jobs
+    def _job(self, i, box):
+        s, d = self.srcs[i], self.dsts[i]
+        return _lib.sb_box_job(d.abi(), s.abi(), _local(box, s))
 
     def _run(self, jobs, params, stream) -> None:
-        for i in range(0, len(jobs), _lib.SB_MAX_BOXES):
-            chunk = jobs[i:i + _lib.SB_MAX_BOXES]
-            arr = (_lib.sb_box_job * len(chunk))(*chunk)
-            _lib.call("sb_lap4_boxes", arr, len(chunk), _lib.d4_constants(self.k),
-                      _lib.launch_of(params, self.extra_flags), stream_ptr(stream))
+        arr = (_lib.sb_box_job * len(jobs))(*jobs)
+        _lib.call("sb_lap4_boxes", arr, len(jobs), _lib.d4_constants(self.k),
+                  _lib.launch_of(params, self.extra_flags), stream_ptr(stream))
 
-    def launch(self, space: IndexSpace | None, params: LaunchParams, stream=None) -> None:
-        self._run(self._jobs(None if space is None else space), params, stream)
 
-    def __call__(self, piece: IndexSpace) -> None:
-        self._run(self._jobs(piece), self.default_params, None)
+class LevelFourthOrderAll(_LevelKernel):
+    """K2 over a level: the ten 4th-order outputs of every box in one launch
+    (``sb_d4_all_boxes``; ``order=2`` selects the 2nd-order set)."""
+
+    site_id = "d4_all_level"
+    space_kind = D4_ALL_SPACE
+    default_params = LaunchParams(32, 4, 4, 2)
+
+    def __init__(self, outs: list[list[DeviceGrid]], srcs: list[DeviceGrid], k: D4Constants, order: int = 4):
+        if len(outs) != len(srcs) or not srcs or any(len(o) != _lib.SB_N_D4_OUT for o in outs):
+            raise UsageError("need ten output grids per src box")
+        if order not in (2, 4):
+            raise UsageError("order must be 2 or 4")
+        for s in srcs:
+            if s.ghost < 2:
+                raise UsageError("the stencils need ghost width >= 2")
+        self.outs, self.srcs, self.k, self.order = [list(o) for o in outs], list(srcs), k, order
+
+    def _boxes(self):
+        return [(s, o) for s, o in zip(self.srcs, self.outs)]
+
+    def _job(self, i, box):
+        s = self.srcs[i]
+        j = _lib.sb_d4_all_job()
+        for a, o in enumerate(self.outs[i]):
+            j.out[a] = o.abi()
+        j.src = s.abi()
+        j.space = _local(box, s)
+        return j
+
+    def _run(self, jobs, params, stream) -> None:
+        arr = (_lib.sb_d4_all_job * len(jobs))(*jobs)
+        _lib.call("sb_d4_all_boxes" if self.order == 4 else "sb_d2_all_boxes", arr, len(jobs),
+                  _lib.d4_constants(self.k), _lib.launch_of(params, self.extra_flags), stream_ptr(stream))
+
+
+class LevelRK4Stage(_LevelKernel):
+    """K5 over a level: one classical RK4 stage (1..4) of the wave equation
+    on every box in one launch (``sb_rk4_stage_boxes``).  ``fields[i]`` is
+    box i's dict of grids phi_s, pi_s, phi0, pi0, acc_phi, acc_pi, phi_out,
+    pi_out (phi_s ghosts filled beforehand, e.g. by LevelGhostSync)."""
+
+    site_id = "rk4_level"
+    space_kind = RK4_SPACE
+    default_params = LaunchParams(64, 4, 16, 1)
+    NAMES = ("phi_s", "pi_s", "phi0", "pi0", "acc_phi", "acc_pi", "phi_out", "pi_out")
+
+    def __init__(self, stage: int, fields: list[dict], c: WaveConstants):
+        if stage not in (1, 2, 3, 4):
+            raise UsageError("stage must be 1..4")
+        if not fields:
+            raise UsageError("need at least one box")
+        self.stage, self.fields, self.c = stage, list(fields), c
+
+    def _boxes(self):
+        return [(f["phi_s"], f) for f in self.fields]
+
+    def _job(self, i, box):
+        f = self.fields[i]
+        j = _lib.sb_rk4_box_job()
+        j.f = _lib.sb_rk4_fields(*[f[n].abi() for n in self.NAMES])
+        j.space = _local(box, f["phi_s"])
+        return j
+
+    def _run(self, jobs, params, stream) -> None:
+        arr = (_lib.sb_rk4_box_job * len(jobs))(*jobs)
+        c = _lib.sb_rk4_constants(_lib.d4_constants(self.c.lap), self.c.half_dt, self.c.dt, self.c.dt6)
+        _lib.call("sb_rk4_stage_boxes", self.stage, arr, len(jobs), c, _lib.launch_of(params, self.extra_flags),
+                  stream_ptr(stream))
 
 
 class LevelGhostSync:

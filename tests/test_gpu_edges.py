@@ -109,8 +109,9 @@ def test_lap7_tiny(n):
     assert same(p.outputs()[0], ref[1:-1, 1:-1, 1:-1])
 
 
-def test_level_with_many_boxes_chunks_launches():
-    """More boxes than SB_MAX_BOXES: the level kernel splits into launches."""
+def test_level_with_more_boxes_than_inline_table():
+    """More boxes than SB_MAX_BOXES: one launch through the device-resident
+    box table."""
     from paper_1308_1343_b200.configs import C4Level
     from paper_1308_1343_b200.level import Box
     boxes = [Box((8 * i, 0, 0), (8 * i + 6, 5, 4 + i % 3)) for i in range(11)]
