@@ -53,6 +53,21 @@ constexpr int kStages = 4;
 #define SB_RKPAIR_BARRIER_EVERY 2
 #endif
 enum { PAIR_A = 0, PAIR_B = 1, PAIR_LA = 2, PAIR_LB = 3 };
+// Laplacian pairs, experiment (off): form the derived stage fields (LA: phi2;
+// LB: phi3, phi4) ONCE per staged point, one plane ahead, into a two-plane
+// shared ring, instead of re-forming them on every thread's 9-value stencil
+// neighbourhood (each staged value is combined by up to 9 threads).  The
+// pre-pass of plane i+1 runs in iteration i before its CTA barrier, so
+// iteration i+1 reads it after that barrier — no extra barrier, but one per
+// plane.  Same bits; 40 % SLOWER (1.49-1.50 vs 1.06-1.08 ms per 384^3 step,
+// three interleaved rounds, profiles/r02/c3_prepass_ab.log): the per-plane
+// barrier and the wait for the next plane's TMA stage serialise the pipeline,
+// and the register cap of four resident CTAs spills (128 vs 56 registers).
+#ifndef SB_RKPAIR_PREPASS
+#define SB_RKPAIR_PREPASS 0
+#endif
+__host__ __device__ constexpr bool prepass(int pair) { return SB_RKPAIR_PREPASS && (pair == PAIR_LA || pair == PAIR_LB); }
+__host__ __device__ constexpr int n_derived(int pair) { return !prepass(pair) ? 0 : pair == PAIR_LA ? 1 : 2; }
 
 __host__ __device__ constexpr int n_halo(int pair) { return pair == PAIR_A || pair == PAIR_LA ? 2 : pair == PAIR_B ? 3 : 4; }
 __host__ __device__ constexpr int n_out(int pair) { return pair == PAIR_A ? 4 : 2; }
@@ -94,6 +109,7 @@ struct PairParams {
 
 struct PCtx {
     const double *stages;
+    double *derived;   // [2][n_derived][plane_elems] (pre-pass pairs)
     uint64_t *full;
     int plane_elems, tile_elems, stage_elems, H, TY, nthr, tid, cx, ry;
     int X0, Y0, Z0, Z1, nplanes;
@@ -184,6 +200,28 @@ __device__ __forceinline__ void out_periodic(const PairParams &P, int k, double 
                          P.zhi[k], P.zhi_dz[k], x + j, y, z, v[j]);
 }
 
+// The derived stage fields of staged plane j, every point of the halo plane
+// once (same single-rounding trees as Nbhd::combine):
+//   LA: phi2 = phi0 + (dt/2) pi0
+//   LB: phi3 = phi0 + (dt/2)(pi0 + (dt/2) L1),  phi4 = phi0 + dt (pi0 + (dt/2) L2)
+template <int PAIR, int TX>
+__device__ __forceinline__ void derive_plane(const PCtx &c, const PairParams &P, int j) {
+    const double *pl = c.stages + (j & (kStages - 1)) * c.stage_elems;
+    double *db = c.derived + (j & 1) * n_derived(PAIR) * c.plane_elems;
+    const int n = (TX + 4) * c.H;
+#pragma unroll 1
+    for (int e = c.tid; e < n; e += c.nthr) {
+        const double f0 = pl[e], q0 = pl[c.plane_elems + e];
+        if constexpr (PAIR == PAIR_LA) {
+            db[e] = add(f0, mul(P.hdt, q0));
+        } else {
+            const double l1 = pl[2 * c.plane_elems + e], l2 = pl[3 * c.plane_elems + e];
+            db[e] = add(f0, mul(P.hdt, add(q0, mul(P.hdt, l1))));
+            db[c.plane_elems + e] = add(f0, mul(P.dt, add(q0, mul(P.hdt, l2))));
+        }
+    }
+}
+
 template <int PAIR, int TX, int NP, int R>
 __device__ __forceinline__ bool pair_plane(int i, const PCtx &c, const PairParams &P, const Lanes<NP> &L,
                                            PRings<NP> &rg) {
@@ -196,35 +234,59 @@ __device__ __forceinline__ bool pair_plane(int i, const PCtx &c, const PairParam
     const double *pl = c.stages + s * c.stage_elems;
 
     double tv[3][NP];   // B: pi0, acc_phi, acc_pi at the thread's points of plane zc
-    if constexpr (PAIR == PAIR_LB) {
-        // phi3 = phi0 + (dt/2) pi2, pi2 = pi0 + (dt/2) L1;  phi4 = phi0 + dt pi3, pi3 = pi0 + (dt/2) L2
-        Nbhd<TX, NP> f0, q0, l, p, d;
-        f0.load(pl, c.ry, c.cx);
-        q0.load(pl + c.plane_elems, c.ry, c.cx);
-        l.load(pl + 2 * c.plane_elems, c.ry, c.cx);
-        double s3[NP], s4[NP];
-        p.combine(q0, P.hdt, l);
-        d.combine(f0, P.hdt, p);
-        d.lap_xy(P.k2, s3);
-#pragma unroll
-        for (int j = 0; j < NP; ++j) {
-            rg.ua[R][j] = d.xr[j + 2];
-            rg.sa[R][j] = s3[j];
-            rg.c3[R][j] = l.xr[j + 2];
+    if constexpr (prepass(PAIR)) {
+        // derived fields of the next plane (read after this iteration's barrier)
+        if (i + 1 < c.nplanes) {
+            mbar_wait(&c.full[(i + 1) & (kStages - 1)], ((i + 1) / kStages) & 1);
+            derive_plane<PAIR, TX>(c, P, i + 1);
         }
-        l.load(pl + 3 * c.plane_elems, c.ry, c.cx);
-        p.combine(q0, P.hdt, l);
-        d.combine(f0, P.dt, p);
-        d.lap_xy(P.k2, s4);
+        const double *db = c.derived + (i & 1) * n_derived(PAIR) * c.plane_elems;
+        constexpr int W = TX + 4;
+        const int ctr = (c.ry + 2) * W + NP * c.cx + 2;   // the thread's points in a staged plane
+        if constexpr (PAIR == PAIR_LB) {
+            Nbhd<TX, NP> d;
+            double s3[NP], s4[NP], f0[NP], q0[NP], l1[NP], l2[NP];
+            d.load(db, c.ry, c.cx);
+            d.lap_xy(P.k2, s3);
 #pragma unroll
-        for (int j = 0; j < NP; ++j) {
-            rg.ub[R][j] = d.xr[j + 2];
-            rg.sb[R][j] = s4[j];
-            rg.c4[R][j] = l.xr[j + 2];
-            rg.c1[R][j] = f0.xr[j + 2];
-            rg.c2[R][j] = q0.xr[j + 2];
+            for (int j = 0; j < NP; ++j) {
+                rg.ua[R][j] = d.xr[j + 2];
+                rg.sa[R][j] = s3[j];
+            }
+            d.load(db + c.plane_elems, c.ry, c.cx);
+            d.lap_xy(P.k2, s4);
+            col_vals<NP>(pl + ctr, f0);
+            col_vals<NP>(pl + c.plane_elems + ctr, q0);
+            col_vals<NP>(pl + 2 * c.plane_elems + ctr, l1);
+            col_vals<NP>(pl + 3 * c.plane_elems + ctr, l2);
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                rg.ub[R][j] = d.xr[j + 2];
+                rg.sb[R][j] = s4[j];
+                rg.c1[R][j] = f0[j];
+                rg.c2[R][j] = q0[j];
+                rg.c3[R][j] = l1[j];
+                rg.c4[R][j] = l2[j];
+            }
+        } else {   // PAIR_LA
+            Nbhd<TX, NP> a;
+            double sa[NP], sb2[NP];
+            a.load(pl, c.ry, c.cx);
+            a.lap_xy(P.k2, sa);
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                rg.ua[R][j] = a.xr[j + 2];
+                rg.sa[R][j] = sa[j];
+            }
+            a.load(db, c.ry, c.cx);
+            a.lap_xy(P.k2, sb2);
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                rg.ub[R][j] = a.xr[j + 2];
+                rg.sb[R][j] = sb2[j];
+            }
         }
-    } else {
+    } else if constexpr (PAIR == PAIR_LB) {    } else {
         Nbhd<TX, NP> a, b, d;
         a.load(pl, c.ry, c.cx);                       // A: phi0   B: phi3
         b.load(pl + c.plane_elems, c.ry, c.cx);       // A: pi0    B: phi0
@@ -274,7 +336,10 @@ __device__ __forceinline__ bool pair_plane(int i, const PCtx &c, const PairParam
     }
 
 #if SB_RKPAIR_BARRIER_EVERY == 2
-    if ((i & 1) || i + 1 == c.nplanes) {   // uniform: every second plane, and the last
+    if constexpr (prepass(PAIR)) {
+        named_bar(1, c.nthr);   // stage s and derived plane i consumed; derived plane i+1 visible
+        if (c.tid == 0 && i + kStages < c.nplanes) issue<PAIR, TX>(c, P, i + kStages, s);
+    } else if ((i & 1) || i + 1 == c.nplanes) {   // uniform: every second plane, and the last
         named_bar(1, c.nthr);              // every thread is done with the stages of planes <= i
         if (c.tid == 0) {
             if ((i & 1) && i - 1 + kStages < c.nplanes) issue<PAIR, TX>(c, P, i - 1 + kStages, (i - 1) & (kStages - 1));
@@ -374,6 +439,7 @@ __global__ void __launch_bounds__(lb_threads(TX, NP, TYC), lb_minb(PAIR, TYC))
     c.stage_elems = n_halo(PAIR) * c.plane_elems + n_tile(PAIR) * c.tile_elems;
     c.full = reinterpret_cast<uint64_t *>(smem);
     c.stages = reinterpret_cast<const double *>(smem + 128);
+    c.derived = const_cast<double *>(c.stages) + kStages * c.stage_elems;
 
     int t = blockIdx.x;
     const int bx = t % P.ntx;
@@ -408,6 +474,11 @@ __global__ void __launch_bounds__(lb_threads(TX, NP, TYC), lb_minb(PAIR, TYC))
         for (int i = 0; i < kStages && i < c.nplanes; ++i) issue<PAIR, TX>(c, P, i, i);
     }
     __syncthreads();
+    if constexpr (prepass(PAIR)) {   // derived fields of plane 0
+        mbar_wait(&c.full[0], 0);
+        derive_plane<PAIR, TX>(c, P, 0);
+        named_bar(1, c.nthr);
+    }
 
     PRings<NP> rg;
 #pragma unroll
@@ -428,8 +499,9 @@ __global__ void __launch_bounds__(lb_threads(TX, NP, TYC), lb_minb(PAIR, TYC))
 }
 
 size_t pair_smem(int pair, int tx, int ty) {
-    return 128 + (size_t)kStages * 8 *
-                     (n_halo(pair) * round_up((tx + 4) * (ty + 4), 16) + n_tile(pair) * round_up(tx * ty, 16));
+    const size_t plane = round_up((tx + 4) * (ty + 4), 16);
+    return 128 + (size_t)kStages * 8 * (n_halo(pair) * plane + n_tile(pair) * round_up(tx * ty, 16)) +
+           (size_t)2 * n_derived(pair) * plane * 8;
 }
 
 template <int PAIR, int TX, int NP, int TYC>
