@@ -17,7 +17,12 @@ observed by the driver's run.
 
 Multi-GPU (torchrun): every rank sweeps its own 256^3 box — independent
 units, no data-path collective — so scaling is weak; the only
-communication is a barrier and the max-over-ranks time.
+communication is a barrier and the max-over-ranks time.  With N > 1 the
+line also carries `zslab`: config 3's 384^3 periodic box cut into N z-slabs
+(one per rank), whose boundary planes cross GPUs every launch — fused into
+the kernels' stores over CUDA-IPC-mapped peer memory (NVLink), and the
+NCCL send/recv baseline — each first checked bit for bit against the
+single-GPU step computed on the same GPU (strong scaling of one box).
 
 `--impl reference` times the reference's algorithm on the host cores, rank 0
 only: each step is one WHOLE 256^3 sweep of config 2, driven by the
@@ -411,6 +416,58 @@ def extra_legs(args, dev: int, stream, hbm_peak: float) -> dict:
     return out
 
 
+def zslab_legs(args, dist, rank: int, world: int, backend: str, dev: int) -> dict:
+    """Config 3 as N z-slabs, one per rank (halo.ZSlabRank, lap_pairs): the
+    fused peer-store exchange and the staged NCCL send/recv baseline."""
+    import torch
+    from paper_1308_1343_b200.configs import C3WaveRK4
+    from paper_1308_1343_b200.halo import ZSlabRank
+    n, g = 384, 2
+    full = C3WaveRK4(n=n).setup()          # the single-GPU step on this rank's GPU: the check
+    full.run()
+    torch.cuda.synchronize()
+    want = (full.rk.phi_b.full().clone(), full.rk.pi_b.full().clone())
+    host_phi, host_pi, c, updates = full.host_phi, full.host_pi, full.c, full.updates
+    del full
+    torch.cuda.empty_cache()
+    modes = [("fused", "device" if backend == "nccl" else "host")]
+    if backend == "nccl":
+        modes.append(("staged", "device"))
+    res = {"box": [n, n, n], "slabs": world, "schedule": "lap_pairs", "scaling": "strong (one box over N GPUs)"}
+    for transport, sync in modes:
+        me = None
+        try:
+            me = ZSlabRank(n, rank, world, g, c, dist, schedule="lap_pairs", transport=transport, sync=sync)
+            me.slab.upload(host_phi, host_pi)
+            torch.cuda.synchronize()
+            dist.barrier()
+            me.step()
+            torch.cuda.synchronize()
+            dist.barrier()
+            z0, nz = me.slab.z0, me.slab.nz
+            ok = bool(torch.equal(me.slab.phi_b.full(), want[0][z0:z0 + nz + 2 * g]) and
+                      torch.equal(me.slab.pi_b.full(), want[1][z0:z0 + nz + 2 * g]))
+            flag = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64,
+                                device="cuda" if backend == "nccl" else "cpu")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            stream = torch.cuda.current_stream()
+            ms, per, clk = _timed_steps(me.step, args.steps, args.warmup, dev, stream)
+            torch.cuda.synchronize()
+            dist.barrier()
+            t = torch.tensor([ms], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            step_ms = float(t.item()) / args.steps
+            res[transport] = {"sync": sync, "bit_exact_vs_single_gpu": bool(flag.item() == 1.0),
+                              "ms_per_step": step_ms, "value": updates / (step_ms * 1e-3) / 1e9, "unit": UNIT,
+                              "gpu_launches_per_step": 2, "exchanges_per_step": 2, "clocks_rank0": clk}
+        except Exception as e:  # noqa: BLE001
+            res[transport] = {"error": repr(e)[:400]}
+        finally:
+            del me
+            torch.cuda.empty_cache()
+    return res
+
+
 def run_ours(args) -> None:
     import torch
 
@@ -550,11 +607,13 @@ def run_ours(args) -> None:
     h2d_bytes, d2h_bytes = prob.h2d_bytes, prob.d2h_bytes
     peaks = measured_peaks()
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    extra = None
+    extra = zslab = None
     if not args.no_extra and world == 1:
         del prob.outs, prob.kernel, prob.src
         torch.cuda.empty_cache()
         extra = extra_legs(args, dev, stream, peak)
+    if not args.no_extra and world > 1:
+        zslab = zslab_legs(args, dist, rank, world, backend, dev)
 
     if rank != 0:
         if dist:
@@ -595,6 +654,7 @@ def run_ours(args) -> None:
         "clocks_e2e": clk_e2e.summary(),
         "sustained": sustained,
         "extra": extra,
+        "zslab": zslab,
     }
     print(json.dumps(out), flush=True)
     if dist:

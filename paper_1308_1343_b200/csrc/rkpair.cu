@@ -59,10 +59,10 @@ enum { PAIR_A = 0, PAIR_B = 1, PAIR_LA = 2, PAIR_LB = 3 };
 // neighbourhood (each staged value is combined by up to 9 threads).  The
 // pre-pass of plane i+1 runs in iteration i before its CTA barrier, so
 // iteration i+1 reads it after that barrier — no extra barrier, but one per
-// plane.  Same bits; 40 % SLOWER (1.49-1.50 vs 1.06-1.08 ms per 384^3 step,
-// three interleaved rounds, profiles/r02/c3_prepass_ab.log): the per-plane
-// barrier and the wait for the next plane's TMA stage serialise the pipeline,
-// and the register cap of four resident CTAs spills (128 vs 56 registers).
+// plane.  Same bits; 11-13 % SLOWER (1.49-1.50 vs 1.32-1.37 ms per 384^3
+// step, three interleaved rounds, profiles/r02/c3_prepass_ab.log): the
+// per-plane barrier and the wait for the next plane's TMA stage serialise the
+// pipeline, and pair LB hits the register cap of four resident CTAs (spills).
 #ifndef SB_RKPAIR_PREPASS
 #define SB_RKPAIR_PREPASS 0
 #endif
@@ -286,7 +286,35 @@ __device__ __forceinline__ bool pair_plane(int i, const PCtx &c, const PairParam
                 rg.sb[R][j] = sb2[j];
             }
         }
-    } else if constexpr (PAIR == PAIR_LB) {    } else {
+    } else if constexpr (PAIR == PAIR_LB) {
+        // phi3 = phi0 + (dt/2) pi2, pi2 = pi0 + (dt/2) L1;  phi4 = phi0 + dt pi3, pi3 = pi0 + (dt/2) L2
+        Nbhd<TX, NP> f0, q0, l, p, d;
+        f0.load(pl, c.ry, c.cx);
+        q0.load(pl + c.plane_elems, c.ry, c.cx);
+        l.load(pl + 2 * c.plane_elems, c.ry, c.cx);
+        double s3[NP], s4[NP];
+        p.combine(q0, P.hdt, l);
+        d.combine(f0, P.hdt, p);
+        d.lap_xy(P.k2, s3);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            rg.ua[R][j] = d.xr[j + 2];
+            rg.sa[R][j] = s3[j];
+            rg.c3[R][j] = l.xr[j + 2];
+        }
+        l.load(pl + 3 * c.plane_elems, c.ry, c.cx);
+        p.combine(q0, P.hdt, l);
+        d.combine(f0, P.dt, p);
+        d.lap_xy(P.k2, s4);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            rg.ub[R][j] = d.xr[j + 2];
+            rg.sb[R][j] = s4[j];
+            rg.c4[R][j] = l.xr[j + 2];
+            rg.c1[R][j] = f0.xr[j + 2];
+            rg.c2[R][j] = q0.xr[j + 2];
+        }
+    } else {
         Nbhd<TX, NP> a, b, d;
         a.load(pl, c.ry, c.cx);                       // A: phi0   B: phi3
         b.load(pl + c.plane_elems, c.ry, c.cx);       // A: pi0    B: phi0

@@ -16,11 +16,27 @@ and two barriers per step instead of four: both outputs of a pair launch
 into the neighbours' ghost planes, since each feeds a stencil of the next
 launch.
 
-* :class:`WaveRK4Slabs` — R slabs in one process (one GPU): the fused
-  exchange exercised end to end without extra GPUs.
-* :class:`ZSlabRank` — one slab per process/rank; neighbour buffers are
-  mapped with CUDA IPC handles exchanged through ``torch.distributed``
-  objects, and ``barrier`` orders the stages across ranks.
+The exchange has two transports:
+
+* ``"fused"`` (default) — the stores above: the boundary planes land in the
+  neighbour's ghost planes from inside the kernel (peer memory);
+* ``"staged"`` — the NCCL baseline: the kernel writes the same boundary
+  planes (with their x/y periodic images) into two local send blocks laid
+  out exactly like a neighbour's g ghost planes, and a transport moves each
+  block into the neighbour's contiguous ghost-plane block — a device copy
+  between slabs of one process, ``ncclSend``/``ncclRecv`` (torch
+  ``batch_isend_irecv``) between ranks.
+
+* :class:`WaveRK4Slabs` — R slabs in one process (one GPU): both transports
+  exercised end to end without extra GPUs.
+* :class:`ZSlabRank` — one slab per process/rank; for ``"fused"`` the
+  neighbour buffers are mapped with CUDA IPC handles exchanged through
+  ``torch.distributed`` objects.  Ranks are ordered between launches either
+  on the host (``sync="host"``: device synchronise + ``dist.barrier``, what
+  ranks sharing one GPU must use) or on the device (``sync="device"``: a
+  one-element all-reduce on the launching stream — it completes on a rank
+  only after every rank's previous kernel has completed, so no host round
+  trip; NCCL only).
 """
 from __future__ import annotations
 
@@ -103,35 +119,90 @@ def _default_params(schedule: str) -> LaunchParams:
     return LaunchParams(64, 4, 16, 1) if schedule == "stages" else LaunchParams(32, 4, 64, 1)
 
 
+TRANSPORTS = ("fused", "staged")
+
+
+def ghost_block(grid: DeviceGrid, side: str):
+    """The g contiguous ghost planes below (``"lo"``) or above (``"hi"``) the
+    interior of `grid`, as a flat view of its storage (whole planes, padding
+    included)."""
+    g, sz, nz = grid.ghost, grid.sz, grid.extents[2]
+    k0 = 0 if side == "lo" else nz + g
+    return grid.storage[k0 * sz:(k0 + g) * sz]
+
+
+class SendBlocks:
+    """Local send blocks of one slab output (staged transport): ``lo`` holds
+    the planes destined for the lower neighbour's upper ghost planes, ``hi``
+    those for the upper neighbour's lower ghost planes; ``targets(nz_lo)``
+    are the (lo, hi) origins to hand the kernel in place of peer origins."""
+
+    def __init__(self, like: DeviceGrid):
+        import torch
+        self.g, self.sz, self.sy, self.xpad = like.ghost, like.sz, like.sy, like.xpad
+        self.lo = torch.empty(self.g * self.sz, dtype=torch.float64, device=like.device)
+        self.hi = torch.empty(self.g * self.sz, dtype=torch.float64, device=like.device)
+
+    def targets(self, nz_lo: int) -> tuple[int, int]:
+        inner = 8 * (self.xpad + self.g * self.sy)   # interior origin of a plane within a block
+        # lower neighbour's planes [nz_lo, nz_lo + g) -> block planes [0, g)
+        lo = self.lo.data_ptr() + inner - 8 * nz_lo * self.sz
+        # upper neighbour's planes [-g, 0) -> block planes [0, g)
+        hi = self.hi.data_ptr() + inner + 8 * self.g * self.sz
+        return lo, hi
+
+
 class WaveRK4Slabs:
     """R z-slabs of one periodic n^3 box in one process.  Each stage launch of
-    slab r writes its boundary planes into slabs r-1 / r+1 (ring)."""
+    slab r writes its boundary planes into slabs r-1 / r+1 (ring): directly
+    (``transport="fused"``) or through its send blocks and a device copy
+    (``"staged"``)."""
 
-    def __init__(self, n: int, parts: int, ghost: int, c: WaveConstants, device=None, schedule: str = "stages"):
+    def __init__(self, n: int, parts: int, ghost: int, c: WaveConstants, device=None, schedule: str = "stages",
+                 transport: str = "fused"):
+        if transport not in TRANSPORTS:
+            raise UsageError(f"unknown z-slab transport {transport!r}")
         self.n, self.g, self.c = n, ghost, c
         self.schedule = schedule
+        self.transport = transport
         self.launches = _launches(schedule)
         cuts = z_cuts(n, parts, ghost)
         self.slabs = [Slab(n, cuts[j], cuts[j + 1] - cuts[j], ghost, device) for j in range(parts)]
         self.params = _default_params(schedule)
+        if transport == "staged":
+            outs = {name for st in self.launches for name in (st[3], st[4] if schedule != "stages" else st[3])}
+            self.send = [{name: SendBlocks(getattr(s, name)) for name in outs} for s in self.slabs]
 
     def upload(self, phi_global, pi_global) -> None:
         for s in self.slabs:
             s.upload(phi_global, pi_global)
 
     def step(self, params: LaunchParams | None = None, stream=None) -> None:
+        import torch
         p = params or self.params
         R = len(self.slabs)
         for stage in self.launches:
             out, out2 = stage[3], stage[4]
+            names = (out,) if self.schedule == "stages" else (out, out2)
             for r, s in enumerate(self.slabs):
                 lo, hi = self.slabs[(r - 1) % R], self.slabs[(r + 1) % R]
-                if self.schedule == "stages":
-                    launch_stage(s, stage, self.c, p, getattr(lo, out).origin_ptr, lo.nz,
-                                 getattr(hi, out).origin_ptr, -s.nz, stream)
+                if self.transport == "staged":
+                    t = [self.send[r][nm].targets(lo.nz) for nm in names]
+                    lo_t, hi_t = tuple(x[0] for x in t), tuple(x[1] for x in t)
                 else:
-                    launch_pair(s, stage, self.c, p, (getattr(lo, out).origin_ptr, getattr(lo, out2).origin_ptr),
-                                lo.nz, (getattr(hi, out).origin_ptr, getattr(hi, out2).origin_ptr), -s.nz, stream)
+                    lo_t = tuple(getattr(lo, nm).origin_ptr for nm in names)
+                    hi_t = tuple(getattr(hi, nm).origin_ptr for nm in names)
+                if self.schedule == "stages":
+                    launch_stage(s, stage, self.c, p, lo_t[0], lo.nz, hi_t[0], -s.nz, stream)
+                else:
+                    launch_pair(s, stage, self.c, p, lo_t, lo.nz, hi_t, -s.nz, stream)
+            if self.transport == "staged":   # every slab's blocks to its neighbours' ghost planes
+                with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream()):
+                    for r in range(R):
+                        lo, hi = self.slabs[(r - 1) % R], self.slabs[(r + 1) % R]
+                        for nm in names:
+                            ghost_block(getattr(lo, nm), "hi").copy_(self.send[r][nm].lo)
+                            ghost_block(getattr(hi, nm), "lo").copy_(self.send[r][nm].hi)
 
     def result(self, name: str = "phi_b", with_ghosts: bool = False):
         import numpy as np
@@ -144,29 +215,39 @@ class WaveRK4Slabs:
 class ZSlabRank:
     """This rank's slab of a z-decomposed periodic box (one slab per rank).
 
-    Neighbour buffers are CUDA-IPC-mapped (peer memory over NVLink on a
-    multi-GPU node); ``dist`` is an initialised ``torch.distributed``
-    module/group for the handle exchange and ``barrier()`` orders stages."""
+    ``transport="fused"``: neighbour buffers are CUDA-IPC-mapped (peer memory
+    over NVLink on a multi-GPU node) and the kernels store the boundary
+    planes into them; ``"staged"``: local send blocks and NCCL send/recv
+    (``dist`` must be an NCCL group).  ``sync="host"`` orders launches with a
+    device synchronise + ``dist.barrier`` (required when ranks share a GPU),
+    ``"device"`` with a one-element all-reduce on the stream (NCCL)."""
 
     def __init__(self, n: int, rank: int, world: int, ghost: int, c: WaveConstants, dist, device=None,
-                 schedule: str = "stages"):
+                 schedule: str = "stages", transport: str = "fused", sync: str = "host"):
         import torch
+        if transport not in TRANSPORTS or sync not in ("host", "device"):
+            raise UsageError(f"bad z-slab transport/sync {transport!r}/{sync!r}")
         self.n, self.g, self.c = n, ghost, c
         self.rank, self.world, self.dist = rank, world, dist
-        self.schedule = schedule
+        self.schedule, self.transport, self.sync = schedule, transport, sync
         self.launches = _launches(schedule)
         cuts = z_cuts(n, world, ghost)
         self.slab = Slab(n, cuts[rank], cuts[rank + 1] - cuts[rank], ghost, device)
         self.params = _default_params(schedule)
+        self.lo, self.hi = (rank - 1) % world, (rank + 1) % world
         shared = ("phi_a", "phi_b") if schedule == "stages" else ("phi_a", "pi_a", "phi_b", "pi_b")
-        mine = {name: (getattr(self.slab, name).storage.untyped_storage()._share_cuda_(),
-                       getattr(self.slab, name).offset) for name in shared}
-        everyone = [None] * world
-        dist.all_gather_object(everyone, (self.slab.nz, mine))
         self._keep = []
         self.peer: dict[tuple[int, str], int] = {}
         self.peer_nz: dict[int, int] = {}
-        for r in {(rank - 1) % world, (rank + 1) % world}:
+        if transport == "fused":
+            mine = {name: (getattr(self.slab, name).storage.untyped_storage()._share_cuda_(),
+                           getattr(self.slab, name).offset) for name in shared}
+        else:
+            mine = {}
+            self.send = {name: SendBlocks(getattr(self.slab, name)) for name in shared}
+        everyone = [None] * world
+        dist.all_gather_object(everyone, (self.slab.nz, mine))
+        for r in {self.lo, self.hi}:
             nz_r, handles = everyone[r]
             self.peer_nz[r] = nz_r
             for name, (h, off) in handles.items():
@@ -177,21 +258,47 @@ class ZSlabRank:
                     self._keep.append(st)
                     ptr = st.data_ptr() + 8 * off
                 self.peer[(r, name)] = ptr
+        if sync == "device":
+            self._token = torch.zeros(1, dtype=torch.float32, device=self.slab.phi0.device)
 
     def barrier(self) -> None:
+        if self.sync == "device":
+            self.dist.all_reduce(self._token)
+            return
         import torch
         torch.cuda.synchronize()
         self.dist.barrier()
 
+    def _exchange(self, names) -> None:
+        """Staged transport: my send blocks to the neighbours' ghost planes and
+        theirs into mine, one grouped NCCL send/recv (sends ordered lo, hi;
+        receives from hi, lo — the order every peer pair matches)."""
+        d = self.dist
+        ops = []
+        for nm in names:
+            grid, blk = getattr(self.slab, nm), self.send[nm]
+            ops += [d.P2POp(d.isend, blk.lo, self.lo), d.P2POp(d.isend, blk.hi, self.hi),
+                    d.P2POp(d.irecv, ghost_block(grid, "hi"), self.hi), d.P2POp(d.irecv, ghost_block(grid, "lo"), self.lo)]
+        for w in d.batch_isend_irecv(ops):
+            w.wait()
+
     def step(self, params: LaunchParams | None = None) -> None:
         p = params or self.params
-        lo, hi = (self.rank - 1) % self.world, (self.rank + 1) % self.world
+        lo, hi = self.lo, self.hi
         for stage in self.launches:
             out, out2 = stage[3], stage[4]
-            if self.schedule == "stages":
-                launch_stage(self.slab, stage, self.c, p, self.peer[(lo, out)], self.peer_nz[lo],
-                             self.peer[(hi, out)], -self.slab.nz)
+            names = (out,) if self.schedule == "stages" else (out, out2)
+            if self.transport == "staged":
+                t = [self.send[nm].targets(self.peer_nz[lo]) for nm in names]
+                lo_t, hi_t = tuple(x[0] for x in t), tuple(x[1] for x in t)
             else:
-                launch_pair(self.slab, stage, self.c, p, (self.peer[(lo, out)], self.peer[(lo, out2)]),
-                            self.peer_nz[lo], (self.peer[(hi, out)], self.peer[(hi, out2)]), -self.slab.nz)
-            self.barrier()
+                lo_t = tuple(self.peer[(lo, nm)] for nm in names)
+                hi_t = tuple(self.peer[(hi, nm)] for nm in names)
+            if self.schedule == "stages":
+                launch_stage(self.slab, stage, self.c, p, lo_t[0], self.peer_nz[lo], hi_t[0], -self.slab.nz)
+            else:
+                launch_pair(self.slab, stage, self.c, p, lo_t, self.peer_nz[lo], hi_t, -self.slab.nz)
+            if self.transport == "staged":
+                self._exchange(names)
+            else:
+                self.barrier()

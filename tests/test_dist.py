@@ -128,5 +128,78 @@ def test_bench_under_torchrun_two_ranks(impl):
     assert rec["value"] > 0 and rec["n_gpus"] == 2
     if impl == "ours":
         assert rec["scaling"] == "weak" and rec["gpu_launches"] == 3
+        # config 3 as two z-slabs, one per rank, halo planes stored into the
+        # other rank's ghost planes through CUDA IPC (host-ordered: ranks share the GPU)
+        zs = rec["zslab"]["fused"]
+        assert zs.get("bit_exact_vs_single_gpu") is True, zs
+        assert zs["ms_per_step"] > 0
     else:
         assert rec["impl"] == "reference"
+
+
+def _device_worker(rank, world, port, n, g, q):
+    """One rank: its shard of the level's boxes swept by the DEVICE kernel
+    (LevelLaplacian4, one launch for the shard), results gathered."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_1308_1343_b200 import _build
+    from paper_1308_1343_b200.grid import DeviceGrid
+    from paper_1308_1343_b200.kernels import LevelLaplacian4
+    _build.build()
+    boxes = level(n)
+    fields = inputs.c4_fields(boxes, g, seed=99)
+    k = inputs.D4Constants.for_spacing(1.0 / n)
+    mine = shard_boxes(boxes, world, rank)
+    srcs, dsts, keys = [], [], []
+    for piece in mine:
+        j = next(i for i, b in enumerate(boxes) if all(b.lo[d] <= piece.lo[d] and piece.hi[d] <= b.hi[d] for d in range(3)))
+        b = boxes[j]
+        # the piece's source with ghosts, cut from its box's field
+        z0, z1 = piece.lo[2] - b.lo[2], piece.hi[2] + 1 - b.lo[2]
+        s = DeviceGrid(piece.extents, g, lower=piece.lo)
+        s.upload(fields[j][z0:z1 + 2 * g])
+        srcs.append(s)
+        dsts.append(DeviceGrid(piece.extents, 0, lower=piece.lo))
+        keys.append((j, z0, z1))
+    LevelLaplacian4(dsts, srcs, k).launch(None, LevelLaplacian4.default_params)
+    results = {key: d.download() for key, d in zip(keys, dsts)}
+    gathered = [None] * world
+    dist.all_gather_object(gathered, results)
+    if rank == 0:
+        q.put(gathered)
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gloo_world2_device_kernels_shard_the_level():
+    """world-size-2 gloo: each rank sweeps its shard of the config-4-style
+    level with the device kernel (ranks share the one GPU; no kernel waits
+    on another rank); the gathered outputs equal the single-box oracle."""
+    import torch.multiprocessing as mp
+    n, g, world = 40, 2, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_device_worker, args=(r, world, port, n, g, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    gathered = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    boxes = level(n)
+    fields = inputs.c4_fields(boxes, g, seed=99)
+    k = inputs.D4Constants.for_spacing(1.0 / n)
+    for j, (b, u) in enumerate(zip(boxes, fields)):
+        nx, ny, nz = b.extents
+        want = np.empty((nz, ny, nx))
+        oracle.lap4(want, u, g, (0, nx, 0, ny, 0, nz), k.k2)
+        got = np.full((nz, ny, nx), np.nan)
+        for part in gathered:
+            for (jj, z0, z1), arr in part.items():
+                if jj == j:
+                    got[z0:z1] = arr
+        assert got.tobytes() == want.tobytes(), j

@@ -21,16 +21,20 @@ def test_z_cuts():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("transport", ["fused", "staged"])
 @pytest.mark.parametrize("schedule", ["stages", "lap_pairs", "pairs"])
 @pytest.mark.parametrize("parts", [1, 2, 3])
-def test_slabs_one_process_match_global_oracle(parts, schedule):
+def test_slabs_one_process_match_global_oracle(parts, schedule, transport):
+    """Fused: the kernels store the boundary planes into the neighbours'
+    ghost planes; staged: into local send blocks that a device copy (NCCL
+    send/recv across ranks) moves there — same bits either way."""
     from paper_1308_1343_b200 import _build
     from paper_1308_1343_b200.halo import WaveRK4Slabs
     _build.build()
     n, g = 24, 2
     phi0, pi0 = inputs.c3_fields(n, g, seed=40 + parts)
     c = inputs.WaveConstants.for_grid(n)
-    sl = WaveRK4Slabs(n, parts, g, c, schedule=schedule)
+    sl = WaveRK4Slabs(n, parts, g, c, schedule=schedule, transport=transport)
     sl.upload(phi0, pi0)
     sl.step()
     wphi, wpi = oracle.rk4_step(phi0, pi0, g, c)
