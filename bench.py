@@ -502,9 +502,9 @@ def run_ours(args) -> None:
         params = LaunchParams(*args.params)
     elif args.tune > 0:
         from paper_1308_1343_b200.traverse import run_loop
-        from paper_1308_1343_b200.tuner import LoopSetup, TopologyConfig, Tuner
+        from paper_1308_1343_b200.tuner import TopologyConfig, Tuner, device_setup
         kern = prob.kernel
-        setup = LoopSetup(kern.site_id, kern.full_space().extents)
+        setup = device_setup(kern)
         tuner = Tuner(TopologyConfig())
         tuner.prime(setup, kern.launch_space(), kern.default_params)
         for _ in range(args.tune):

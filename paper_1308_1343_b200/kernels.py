@@ -67,6 +67,38 @@ class DeviceKernel:
     def full_space(self) -> IndexSpace:
         raise NotImplementedError
 
+    def pitch_class(self) -> int:
+        """Row pitch (elements) of the swept source grid: part of the device
+        tuning key (tuner.device_setup)."""
+        for name in ("src", "srcs", "ins", "fields"):
+            g = getattr(self, name, None)
+            if g is None:
+                continue
+            if isinstance(g, list):
+                g = g[0]["phi_s"] if isinstance(g[0], dict) else g[0]
+            return g.sy
+        return 0
+
+    # host-path caches: the ctypes argument structs of a launch are built once
+    # per (space, params) — the grids of a kernel object never move
+    def _space_arg(self, space: IndexSpace, grid: DeviceGrid) -> _lib.sb_space:
+        cache = self.__dict__.setdefault("_space_cache", {})
+        key = (tuple(space.lo), tuple(space.hi))
+        a = cache.get(key)
+        if a is None:
+            if len(cache) > 256:
+                cache.clear()
+            a = cache[key] = _local(space, grid)
+        return a
+
+    def _launch_arg(self, params: LaunchParams, flags: int = 0) -> _lib.sb_launch:
+        cache = self.__dict__.setdefault("_launch_cache", {})
+        key = (params, flags | self.extra_flags)
+        a = cache.get(key)
+        if a is None:
+            a = cache[key] = _lib.launch_of(params, flags | self.extra_flags)
+        return a
+
 
 class Laplacian7(DeviceKernel):
     """K1 — ``_update_rows`` (stencil.py:31-39): dst = C0*b + C1*(sum of 6 neighbours)."""
@@ -82,13 +114,14 @@ class Laplacian7(DeviceKernel):
         if dst.lower != src.lower or dst.extents != src.extents:
             raise UsageError("dst and src must cover the same box")
         self.dst, self.src, self.c0, self.c1 = dst, src, float(c0), float(c1)
+        self._abi = (dst.abi(), src.abi())
 
     def full_space(self) -> IndexSpace:
         return _interior_space(self.src)
 
     def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
-        _lib.call("sb_lap7", self.dst.abi(), self.src.abi(), _local(space, self.src), self.c0, self.c1,
-                  _lib.launch_of(params, self.extra_flags), stream_ptr(stream))
+        _lib.call("sb_lap7", self._abi[0], self._abi[1], self._space_arg(space, self.src), self.c0, self.c1,
+                  self._launch_arg(params), stream_ptr(stream))
 
     def iterate(self, a: DeviceGrid, b: DeviceGrid, space: IndexSpace, iters: int,
                 params: LaunchParams | None = None, stream=None) -> DeviceGrid:
@@ -122,8 +155,10 @@ class FourthOrderAll(DeviceKernel):
         return _interior_space(self.src)
 
     def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
-        _lib.call("sb_d4_all", self._out_abi, self.src.abi(), _local(space, self.src), _lib.d4_constants(self.k),
-                  _lib.launch_of(params, self.extra_flags), stream_ptr(stream))
+        if not hasattr(self, "_src_abi"):
+            self._src_abi, self._k_abi = self.src.abi(), _lib.d4_constants(self.k)
+        _lib.call("sb_d4_all", self._out_abi, self._src_abi, self._space_arg(space, self.src), self._k_abi,
+                  self._launch_arg(params), stream_ptr(stream))
 
     def run_host(self, host_in_ptr: int, host_out_ptrs: list[int], params: LaunchParams | None = None,
                  chunk: int = 32) -> None:
@@ -172,8 +207,10 @@ class SecondOrderAll(FourthOrderAll):
     site_id = "d2_all"
 
     def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
-        _lib.call("sb_d2_all", self._out_abi, self.src.abi(), _local(space, self.src), _lib.d4_constants(self.k),
-                  _lib.launch_of(params, self.extra_flags), stream_ptr(stream))
+        if not hasattr(self, "_src_abi"):
+            self._src_abi, self._k_abi = self.src.abi(), _lib.d4_constants(self.k)
+        _lib.call("sb_d2_all", self._out_abi, self._src_abi, self._space_arg(space, self.src), self._k_abi,
+                  self._launch_arg(params), stream_ptr(stream))
 
 
 class Laplacian4(DeviceKernel):
@@ -201,6 +238,15 @@ def _clip(box: IndexSpace, space) -> IndexSpace | None:
     lo = tuple(max(a, b) for a, b in zip(box.lo, space.lo))
     hi = tuple(min(a, b) for a, b in zip(box.hi, space.hi))
     return None if any(h <= l for l, h in zip(lo, hi)) else IndexSpace(lo, hi)
+
+
+def _array_of(owner, ctype, jobs):
+    """The ctypes array of a (cached) job list, built once per list."""
+    cache = owner.__dict__.setdefault("_array_cache", {})
+    a = cache.get(id(jobs))
+    if a is None or a[0] is not jobs:
+        a = cache[id(jobs)] = (jobs, (ctype * len(jobs))(*jobs))
+    return a[1]
 
 
 class _LevelKernel(DeviceKernel):
@@ -236,7 +282,14 @@ class _LevelKernel(DeviceKernel):
         return jobs
 
     def launch(self, space: IndexSpace | None, params: LaunchParams, stream=None) -> None:
-        jobs = self._jobs(space)
+        cache = self.__dict__.setdefault("_jobs_cache", {})
+        key = None if space is None else (tuple(space.lo), tuple(space.hi))
+        jobs = cache.get(key)
+        if jobs is None:
+            if len(cache) > 256:
+                cache.clear()
+                self.__dict__.pop("_array_cache", None)
+            jobs = cache[key] = self._jobs(space)
         if jobs:
             self._run(jobs, params, stream)
 
@@ -268,9 +321,9 @@ class LevelLaplacian4(_LevelKernel):
         return _lib.sb_box_job(d.abi(), s.abi(), _local(box, s))
 
     def _run(self, jobs, params, stream) -> None:
-        arr = (_lib.sb_box_job * len(jobs))(*jobs)
-        _lib.call("sb_lap4_boxes", arr, len(jobs), _lib.d4_constants(self.k),
-                  _lib.launch_of(params, self.extra_flags), stream_ptr(stream))
+        arr = _array_of(self, _lib.sb_box_job, jobs)
+        _lib.call("sb_lap4_boxes", arr, len(jobs), _lib.d4_constants(self.k), self._launch_arg(params),
+                  stream_ptr(stream))
 
 
 class LevelFourthOrderAll(_LevelKernel):
@@ -304,9 +357,9 @@ class LevelFourthOrderAll(_LevelKernel):
         return j
 
     def _run(self, jobs, params, stream) -> None:
-        arr = (_lib.sb_d4_all_job * len(jobs))(*jobs)
+        arr = _array_of(self, _lib.sb_d4_all_job, jobs)
         _lib.call("sb_d4_all_boxes" if self.order == 4 else "sb_d2_all_boxes", arr, len(jobs),
-                  _lib.d4_constants(self.k), _lib.launch_of(params, self.extra_flags), stream_ptr(stream))
+                  _lib.d4_constants(self.k), self._launch_arg(params), stream_ptr(stream))
 
 
 class LevelRK4Stage(_LevelKernel):
@@ -338,7 +391,7 @@ class LevelRK4Stage(_LevelKernel):
         return j
 
     def _run(self, jobs, params, stream) -> None:
-        arr = (_lib.sb_rk4_box_job * len(jobs))(*jobs)
+        arr = _array_of(self, _lib.sb_rk4_box_job, jobs)
         c = _lib.sb_rk4_constants(_lib.d4_constants(self.c.lap), self.c.half_dt, self.c.dt, self.c.dt6)
         _lib.call("sb_rk4_stage_boxes", self.stage, arr, len(jobs), c, _lib.launch_of(params, self.extra_flags),
                   stream_ptr(stream))

@@ -12,14 +12,14 @@ the sweep.  Index spaces are the reference's array indices
 """
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 
 from .grid import DeviceGrid
 from .kernels import Laplacian7
 from .traverse import IndexSpace, _Timer, run_loop, run_static
-from .tuner import LoopSetup, TopologyConfig, Tuner
+from .tuner import TopologyConfig, Tuner, device_setup
 
 C0 = -6.0 / 8.0
 C1 = 1.0 / 8.0
@@ -75,14 +75,21 @@ def run_naive(n: int, iters: int, seed: int, n_threads: int, c0: float = C0, c1:
 
 
 def run_tuned(n: int, iters: int, seed: int, topo: TopologyConfig, c0: float = C0,
-              c1: float = C1) -> tuple[StencilRun, Tuner]:
+              c1: float = C1, graphed: bool = True) -> tuple[StencilRun, Tuner]:
+    """stencil.py:80-94 on the device.  The tuning key adds the grid pitch and
+    SM count (tuner.device_setup); with ``graphed`` (default) every tuned
+    execution replays a per-launch-shape CUDA graph, so the tuner times the
+    sweep itself, not the host launch path (traverse.run_loop)."""
     src, dst = _buffers(n, seed)
     out = StencilRun(np.empty(0))
     space = _space(n)
-    setup = LoopSetup("laplacian3d", space.extents, "vector", topo.n_coarse_threads, topo.n_fine_threads)
+    k_ab, k_ba = Laplacian7(dst, src, c0, c1), Laplacian7(src, dst, c0, c1)
+    setup = replace(device_setup(k_ab, space.extents), n_coarse_threads=topo.n_coarse_threads,
+                    n_fine_threads=topo.n_fine_threads)
     tuner = Tuner(topo)
     for _ in range(iters):
-        out.iter_seconds.append(run_loop(setup, space, Laplacian7(dst, src, c0, c1), tuner))
+        out.iter_seconds.append(run_loop(setup, space, k_ab, tuner, graphed=graphed))
+        k_ab, k_ba = k_ba, k_ab
         src, dst = dst, src
     out.final = src.download(with_ghosts=True)
     return out, tuner

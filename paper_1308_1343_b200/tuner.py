@@ -105,13 +105,21 @@ class TopologyConfig:
 
 @dataclass(frozen=True)
 class LoopSetup:
-    """Tuning identity (reference tuner.py:78-96); equal setups share history."""
+    """Tuning identity (reference tuner.py:78-96); equal setups share history.
+
+    Device setups add what changes the best launch shape on a GPU beside the
+    extents: the row pitch of the swept source grid (``pitch``,
+    elements; 0 = not a device setup) and the device's SM count
+    (``sm_count``).  Both default to 0, so the reference's CPU setups, their
+    RNG seeds and logs are unchanged; ``device_setup`` builds a device key."""
 
     site_id: str
     extents: tuple[int, ...]
     alignment: str = "vector"   # none | vector | cache_line
     n_coarse_threads: int = 1
     n_fine_threads: int = 1
+    pitch: int = 0
+    sm_count: int = 0
 
     def __post_init__(self) -> None:
         if any(e <= 0 for e in self.extents):
@@ -122,6 +130,25 @@ class LoopSetup:
     @property
     def dim(self) -> int:
         return len(self.extents)
+
+
+def _rng_key(seed: int, setup: LoopSetup) -> str:
+    """Per-setup RNG stream key (reference tuner.py:387); device setups also
+    key on pitch and SM count."""
+    k = f"{seed}:{setup.site_id}:{setup.extents}"
+    if setup.pitch or setup.sm_count:
+        k += f":{setup.pitch}:{setup.sm_count}"
+    return k
+
+
+def device_setup(kernel, extents=None) -> LoopSetup:
+    """The LoopSetup of a device kernel: site, extents (default: the kernel's
+    full space), the row pitch of its swept source grid and the SM count of
+    the current device."""
+    import torch
+    ext = tuple(extents) if extents is not None else kernel.full_space().extents
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    return LoopSetup(kernel.site_id, ext, pitch=int(kernel.pitch_class()), sm_count=int(sms))
 
 
 @dataclass(frozen=True)
@@ -514,7 +541,7 @@ class Tuner:
         st = self._states.get(setup)
         if st is None:
             sp = space if space is not None else self.default_space
-            rng = random.Random(f"{self.topo.rng_seed}:{setup.site_id}:{setup.extents}")
+            rng = random.Random(_rng_key(self.topo.rng_seed, setup))
             start = sp.initial(setup, self.topo)
             if self.cache is not None:
                 cached = self.cache.get(setup, sp)
@@ -530,7 +557,7 @@ class Tuner:
         if setup in self._states:
             return
         space.check(start, setup, self.topo)
-        rng = random.Random(f"{self.topo.rng_seed}:{setup.site_id}:{setup.extents}")
+        rng = random.Random(_rng_key(self.topo.rng_seed, setup))
         self._states[setup] = _State(rng=rng, space=space, current=start)
 
     def space_of(self, setup: LoopSetup):
@@ -629,7 +656,10 @@ class TuningCache:
                 self._d = {}
 
     def _key(self, setup: LoopSetup) -> str:
-        return f"{self.device_key}|{setup.site_id}|{'x'.join(map(str, setup.extents))}"
+        k = f"{self.device_key}|{setup.site_id}|{'x'.join(map(str, setup.extents))}"
+        if setup.pitch or setup.sm_count:
+            k += f"|sy{setup.pitch}|sm{setup.sm_count}"
+        return k
 
     def get(self, setup: LoopSetup, space):
         if not isinstance(space, LaunchSpace):
