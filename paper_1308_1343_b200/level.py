@@ -9,6 +9,13 @@ integer logic and out of scope.
 
 :func:`boxes_of` accepts any object with ``to_bboxes()`` (the reference's
 ``BBoxSet``), a list of reference ``BBox`` objects, or a list of :class:`Box`.
+Strided (coarsened) levels — ``BBoxSet.coarsen`` (bboxset.py:387-406), whose
+boxes hold the points ``offset + k * stride`` — are swept in compact lattice
+coordinates (:func:`compact_level`): a grid function on a strided box is
+stored one value per lattice point, the stencil's neighbours at +-stride are
+the compact neighbours at +-1, and the spacing is ``h * stride``; the kernels
+are unchanged.  ``as_box`` keeps rejecting strided boxes exactly like the
+reference's ``index_space_from_bbox`` (traverse.py:63-64).
 :func:`box_difference` produces, for the single-box-minus-box case config 4
 uses, the same sorted slab decomposition the reference returns (outermost
 dimension split first; verified against the reference in
@@ -85,6 +92,49 @@ def boxes_of(level) -> list[Box]:
     """Canonical box list of a level: ``level.to_bboxes()`` or an iterable."""
     raw = level.to_bboxes() if hasattr(level, "to_bboxes") else list(level)
     return [b for b in (as_box(x) for x in raw) if not b.is_empty]
+
+
+@dataclass(frozen=True)
+class Lattice:
+    """The sub-lattice ``offset + k * stride`` of a strided level and the map
+    between its fine coordinates and compact coordinates k."""
+
+    stride: tuple[int, ...]
+    offset: tuple[int, ...]
+
+    def to_compact(self, p) -> tuple[int, ...]:
+        out = []
+        for x, o, st in zip(p, self.offset, self.stride):
+            if (x - o) % st:
+                raise UsageError(f"point {tuple(p)} is not on the lattice {self}")
+            out.append((x - o) // st)
+        return tuple(out)
+
+    def to_fine(self, k) -> tuple[int, ...]:
+        return tuple(o + c * st for c, o, st in zip(k, self.offset, self.stride))
+
+
+def compact_level(level) -> tuple[list[Box], Lattice]:
+    """The boxes of a (possibly strided) level in compact lattice coordinates
+    and the lattice: ``level.to_bboxes()`` (or a list of reference BBoxes
+    sharing one stride and anchor, bboxset.py:240-263).  Unit-stride levels
+    come back unchanged with a unit lattice."""
+    raw = [b for b in (level.to_bboxes() if hasattr(level, "to_bboxes") else list(level)) if not b.is_empty]
+    if not raw:
+        return [], Lattice((1, 1, 1), (0, 0, 0))
+    stride = tuple(getattr(raw[0].stride, "steps", getattr(raw[0].stride, "coords", None)))
+    if hasattr(level, "offset"):
+        offset = tuple(o % st for o, st in zip(level.offset.coords, stride))
+    else:
+        offset = tuple(l % st for l, st in zip(raw[0].lower.coords, stride))
+    lat = Lattice(stride, offset)
+    boxes = []
+    for b in raw:
+        st = tuple(getattr(b.stride, "steps", getattr(b.stride, "coords", None)))
+        if st != stride:
+            raise UsageError("a level's boxes must share one stride")
+        boxes.append(Box(lat.to_compact(b.lower.coords), lat.to_compact(b.upper.coords)))
+    return boxes, lat
 
 
 def box_difference(a: Box, b: Box) -> list[Box]:
