@@ -158,6 +158,11 @@ SB_API int sb_abi_version(void);
 SB_API const char *sb_last_error(void);
 SB_API int sb_init(int device);
 SB_API int sb_get_device_info(sb_device_info *info);
+/* Let kernels on the current device load/store the memory of device `peer`
+ * (NVLink peer access; the z-slab halo stores into a neighbour GPU's ghost
+ * planes).  SB_OK if enabled, already enabled or peer is the current device;
+ * SB_RESOURCE if the devices cannot be peers. */
+SB_API int sb_enable_peer_access(int peer);
 
 /* K0 — vlanes.forward_difference (vlanes.py:342-349) when kind == 0:
  * dst[i] = src[i+1] - src[i], 0 <= i < n-1;  vlanes.centered_difference

@@ -168,6 +168,21 @@ int sb_init(int device) {
     return reserve_barrier_counters(device);
 }
 
+int sb_enable_peer_access(int peer) {
+    int dev = 0;
+    if (int rc = check_cuda(cudaGetDevice(&dev), "cudaGetDevice")) return rc;
+    if (peer == dev) return SB_OK;
+    int can = 0;
+    if (int rc = check_cuda(cudaDeviceCanAccessPeer(&can, dev, peer), "cudaDeviceCanAccessPeer")) return rc;
+    if (!can) return fail(SB_RESOURCE, "enable_peer_access: the current device cannot access the peer device");
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();   // clear the sticky-free "already enabled" status
+        return SB_OK;
+    }
+    return check_cuda(e, "cudaDeviceEnablePeerAccess");
+}
+
 int sb_get_device_info(sb_device_info *info) {
     if (!info) return fail(SB_USAGE, "null info");
     int dev = 0;

@@ -257,6 +257,11 @@ class ZSlabRank:
                     st = torch.UntypedStorage._new_shared_cuda(*h)
                     self._keep.append(st)
                     ptr = st.data_ptr() + 8 * off
+                    # our kernels store into the neighbour's memory: peer
+                    # access from OUR device to the owner's (a no-op when the
+                    # ranks share a GPU)
+                    with torch.cuda.device(self.slab.phi0.device):
+                        _lib.call("sb_enable_peer_access", st.device.index)
                 self.peer[(r, name)] = ptr
         if sync == "device":
             self._token = torch.zeros(1, dtype=torch.float32, device=self.slab.phi0.device)
