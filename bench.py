@@ -20,9 +20,10 @@ units, no data-path collective — so scaling is weak; the only
 communication is a barrier and the max-over-ranks time.  With N > 1 the
 line also carries `zslab`: config 3's 384^3 periodic box cut into N z-slabs
 (one per rank), whose boundary planes cross GPUs every launch — fused into
-the kernels' stores over CUDA-IPC-mapped peer memory (NVLink), and the
-NCCL send/recv baseline — each first checked bit for bit against the
-single-GPU step computed on the same GPU (strong scaling of one box).
+the kernels' stores over CUDA-IPC-mapped peer memory (NVLink), and with
+--zslab-staged the NCCL send/recv baseline — each first checked bit for bit
+against the single-GPU step computed on the same GPU (strong scaling of one
+box).
 
 `--impl reference` times the reference's algorithm on the host cores, rank 0
 only: each step is one WHOLE 256^3 sweep of config 2, driven by the
@@ -431,7 +432,7 @@ def zslab_legs(args, dist, rank: int, world: int, backend: str, dev: int) -> dic
     del full
     torch.cuda.empty_cache()
     modes = [("fused", "device" if backend == "nccl" else "host")]
-    if backend == "nccl":
+    if backend == "nccl" and args.zslab_staged:   # opt-in: NCCL point-to-point exchange baseline
         modes.append(("staged", "device"))
     res = {"box": [n, n, n], "slabs": world, "schedule": "lap_pairs", "scaling": "strong (one box over N GPUs)"}
     for transport, sync in modes:
@@ -676,7 +677,10 @@ def main(argv=None):
     ap.add_argument("--ref-seconds", dest="ref_seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds-1t", dest="ref_seconds_1t", type=float, default=5.0)
     ap.add_argument("--no-cpu", dest="no_cpu", action="store_true")
-    ap.add_argument("--no-extra", dest="no_extra", action="store_true", help="skip the config 1/3/4/5 legs")
+    ap.add_argument("--no-extra", dest="no_extra", action="store_true",
+                    help="skip the config 1/3/4/5 legs (N=1) and the config-3 z-slab legs (N>1)")
+    ap.add_argument("--zslab-staged", dest="zslab_staged", action="store_true",
+                    help="N>1: also time the z-slab exchange as NCCL send/recv of staged boundary planes")
     ap.add_argument("--sustained-steps", dest="sustained_steps", type=int, default=3000,
                     help="extra back-to-back steps timed after the main region (0 = skip)")
     args = ap.parse_args(argv)
