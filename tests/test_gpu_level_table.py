@@ -198,3 +198,45 @@ def test_table_capture_rules_and_release():
     _lib.call("sb_release_tables")
     kern.launch(None, LaunchParams(64, 4, 8, 2))
     torch.cuda.synchronize()
+
+
+def test_multi_box_error_paths():
+    """Periodic refresh and z-slab stores are single-box operations; bad
+    tables are usage errors, not crashes."""
+    import ctypes as C
+    from paper_1308_1343_b200.kernels import LevelRK4Stage
+    boxes = random_level(10, 31, region=(30, 20, 20))
+    c = inputs.WaveConstants.for_grid(32)
+    fields = [{name: DeviceGrid(b.extents, G if name == "phi_s" else 0, lower=b.lo)
+               for name in LevelRK4Stage.NAMES} for b in boxes]
+    kern = LevelRK4Stage(2, fields, c)
+    kern.extra_flags = _lib.SB_LAUNCH_PERIODIC_GHOSTS
+    with pytest.raises(UsageError):
+        kern.launch(None, LaunchParams(64, 4, 8, 1))
+    with pytest.raises(UsageError):
+        _lib.call("sb_lap4_boxes", None, 3, _lib.sb_d4_constants(1, 1, 1), _lib.launch(32, 4, 8), 0)
+    assert _lib.load().sb_lap4_boxes(None, 0, _lib.sb_d4_constants(1, 1, 1), _lib.launch(32, 4, 8), None) == 0
+
+
+def test_boxes_with_empty_spaces_are_skipped(monkeypatch):
+    """A level sweep clipped to a space that misses most boxes: only the
+    touched boxes' points change, still one launch."""
+    from paper_1308_1343_b200.kernels import LevelLaplacian4
+    from paper_1308_1343_b200.traverse import IndexSpace
+    boxes = random_level(24, 41, region=(60, 40, 30), origin=(0, 0, 0))
+    srcs, host = grids(boxes, 42)
+    dsts = [DeviceGrid(b.extents, 0, lower=b.lo).fill_(7.0) for b in boxes]
+    k = inputs.D4Constants.for_spacing(0.05)
+    kern = LevelLaplacian4(dsts, srcs, k)
+    space = IndexSpace((5, 3, 2), (33, 21, 15))
+    cnt = Counter(monkeypatch)
+    kern.launch(space, LaunchParams(32, 4, 4, 2))
+    assert sum(cnt.n.values()) == 1
+    for b, u, d in zip(boxes, host, dsts):
+        nx, ny, nz = b.extents
+        want = np.full((nz, ny, nx), 7.0)
+        lo = [max(b.lo[i], space.lo[i]) - b.lo[i] for i in range(3)]
+        hi = [min(b.hi[i] + 1, space.hi[i]) - b.lo[i] for i in range(3)]
+        if all(h > l for l, h in zip(lo, hi)):
+            oracle.lap4(want, u, G, (lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]), k.k2)
+        assert d.download().tobytes() == want.tobytes(), b
