@@ -124,3 +124,22 @@ def test_c5_whole_volume_all_24_outputs():
     oracle.run_static(planes, 0, n, _threads())
     for o, got in enumerate(p.outputs()):
         _same(got, want[o], f"C5 output {o}")
+
+
+def test_c2_second_order_set_whole_volume():
+    """north_star (c)'s 2nd-order operator set (sb_d2_all) over the whole
+    256^3 box, all ten outputs."""
+    from paper_1308_1343_b200.grid import DeviceGrid
+    from paper_1308_1343_b200.kernels import SecondOrderAll
+    n, g = 256, 2
+    u = inputs.c2_field(n, g)
+    k = inputs.D2Constants.for_spacing(1.0 / n)
+    src = DeviceGrid((n,) * 3, g)
+    src.upload(u, with_ghosts=True)
+    outs = [DeviceGrid((n,) * 3, 0) for _ in range(10)]
+    kern = SecondOrderAll(outs, src, k)
+    kern.launch(kern.full_space(), kern.default_params)
+    want = [np.empty((n, n, n)) for _ in range(10)]
+    oracle.run_static(lambda z0, z1: oracle.d2_all(want, u, g, (0, n, 0, n, z0, z1), k), 0, n, _threads())
+    for i, o in enumerate(outs):
+        _same(o.download(), want[i], f"C2 order-2 {inputs.C2_OUTPUT_NAMES[i]}")
