@@ -293,7 +293,8 @@ def run_reference(args) -> None:
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (seeded host generator, BASELINE.json config 2 shapes)",
-           "config": dict(WORKLOAD, parallelism=f"host threads x{cpu.threads}", input_sha256=cpu.sha),
+           "config": dict(WORKLOAD, input_sha256=cpu.sha),
+           "impl_config": {"parallelism": f"host threads x{cpu.threads}", "engine": cpu.engine_name},
            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu.threads, "kind": "port", "cpu_model": cpu_model(),
                             "engine": cpu.engine_name,
                             "sample": f"each step: one whole 256^3 sweep (all ten outputs) through {cpu.engine_name} "
@@ -637,9 +638,12 @@ def run_ours(args) -> None:
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded host generator, BASELINE.json config 2 shapes)",
-        "config": dict(WORKLOAD, parallelism=f"box-per-rank x{world}", input_sha256=inputs.sha256(prob.host_u),
-                       launch={"tile_x": params.tile_x, "tile_y": params.tile_y, "z_chunk": params.z_chunk,
-                               "points_per_thread": params.points_per_thread}, tuning=tune_info),
+        # `config` is the workload only (identical in both arms); how this arm
+        # ran it is in `impl_config`
+        "config": dict(WORKLOAD, input_sha256=inputs.sha256(prob.host_u)),
+        "impl_config": {"parallelism": f"box-per-rank x{world}",
+                        "launch": {"tile_x": params.tile_x, "tile_y": params.tile_y, "z_chunk": params.z_chunk,
+                                   "points_per_thread": params.points_per_thread}, "tuning": tune_info},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic,
                      "traffic_source": "ncu --set full, profiles/ncu_summary.json (builder capture, not this run)",
