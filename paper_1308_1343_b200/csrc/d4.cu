@@ -564,6 +564,7 @@ struct DevTable {
 };
 std::mutex g_tab_mu;
 std::map<std::pair<int, std::string>, DevTable> g_tables;
+constexpr size_t kMaxTables = 4096;   // (level shape, launch shape) pairs kept per process
 
 void put(std::string &k, const void *p, size_t n) { k.append(static_cast<const char *>(p), n); }
 void put_array(std::string &k, const sb_array &a) {
@@ -596,6 +597,16 @@ int box_table(int mode, const D4Job *jobs, const std::vector<int> &live, int TX,
         if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
             return fail(SB_USAGE, "box table: first launch of this level shape inside a CUDA-graph capture "
                                   "(launch it once before capturing)");
+        if (g_tables.size() >= kMaxTables) {   // bound the cache: start over (waits for the device)
+            if (int rc = check_cuda(cudaDeviceSynchronize(), "box table cache reset (wait)")) return rc;
+            int cur = dev;
+            for (auto &kv : g_tables) {
+                cudaSetDevice(kv.first.first);
+                cudaFree(kv.second.buf);
+            }
+            cudaSetDevice(cur);
+            g_tables.clear();
+        }
         std::vector<BoxDesc> boxes(nb);
         std::vector<PwDesc> pws(npw ? nb : 0);
         std::vector<int> begin(nb);
