@@ -277,6 +277,103 @@ int phaseb2_launch_t(const double *ops, const Term *table, double *out, int bloc
     return (int)cudaGetLastError();
 }
 
+// SRC 5 — the configuration a 64-point config-5 phase B would use: 64 points
+// per CTA, two per lane (a warp covers the tile), ONE output per warp at a
+// time; operands 0..127 in TMEM (columns 4j..4j+3 hold points 2l, 2l+1 of
+// lane l, replicated in all four subpartitions), operands 128..239 in shared
+// memory ([112][64], LDS.128); the term table packed as in rhs24.cu (eight
+// terms per five 16-byte words, broadcast reads) with p, q in 0..239 — every
+// operand comes from TMEM or shared memory by a warp-uniform branch.
+constexpr int NPT5 = 64, NSM5 = NOPS - NTM_OPS;
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+    phaseb5_kernel(const double *ops /*[NOPS][NPT5]*/, const uint4 *table /*[NOUT][40]*/, double *out, int reps) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    uint32_t *slot = reinterpret_cast<uint32_t *>(smem);
+    uint4 *tt = reinterpret_cast<uint4 *>(smem + 128);
+    double *sv = reinterpret_cast<double *>(smem + 128 + sizeof(uint4) * NOUT * 40);   // [NSM5][NPT5]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, sp = warp & 3;
+    const int pt = 2 * lane;
+    if (warp == 0) tmem_alloc(slot, 512);
+    for (int e = threadIdx.x; e < NOUT * 40; e += NW * 32) tt[e] = table[e];
+    for (int e = threadIdx.x; e < NSM5 * NPT5; e += NW * 32) sv[e] = ops[NTM_OPS * NPT5 + e];
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tb = *slot;
+    const uint32_t lanebits = tb + ((uint32_t)(32 * sp) << 16);
+    for (int j = warp >> 2; j < NTM_OPS; j += NW / 4) {
+        const unsigned long long a = __double_as_longlong(ops[j * NPT5 + pt]);
+        const unsigned long long b = __double_as_longlong(ops[j * NPT5 + pt + 1]);
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(lanebits + 4 * j),
+                     "r"((uint32_t)a), "r"((uint32_t)(a >> 32)), "r"((uint32_t)b), "r"((uint32_t)(b >> 32))
+                     : "memory");
+    }
+    tmem_wait_st();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t svb = smem_u32(sv) + 8 * pt - NTM_OPS * (NPT5 * 8);
+    for (int r = 0; r < reps; ++r) {
+        for (int o = warp; o < NOUT; o += NW) {
+            const uint4 *T = tt + o * 40;
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll 1
+            for (int g = 0; g < 8; ++g) {
+                const double2 c01 = *reinterpret_cast<const double2 *>(T + 5 * g);
+                const double2 c23 = *reinterpret_cast<const double2 *>(T + 5 * g + 1);
+                const double2 c45 = *reinterpret_cast<const double2 *>(T + 5 * g + 2);
+                const double2 c67 = *reinterpret_cast<const double2 *>(T + 5 * g + 3);
+                const uint4 w = T[5 * g + 4];
+                const double cf[8] = {c01.x, c01.y, c23.x, c23.y, c45.x, c45.y, c67.x, c67.y};
+                const uint32_t pq[8] = {w.x & 0xffffu, w.x >> 16, w.y & 0xffffu, w.y >> 16,
+                                        w.z & 0xffffu, w.z >> 16, w.w & 0xffffu, w.w >> 16};
+                uint32_t tw[16][4];
+                double2 v[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const uint32_t op = (k & 1) ? (pq[k >> 1] >> 8) : (pq[k >> 1] & 0xffu);
+                    if (op < NTM_OPS) ld_x4(lanebits + 4 * op, tw[k]);
+                    else v[k] = lds128(svb + op * (NPT5 * 8));
+                }
+                tmem_wait_ld();
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const uint32_t op = (k & 1) ? (pq[k >> 1] >> 8) : (pq[k >> 1] & 0xffu);
+#pragma unroll
+                    for (int n = 0; n < 4; ++n) pin(tw[k][n]);
+                    if (op < NTM_OPS) {
+                        v[k].x = __hiloint2double((int)tw[k][1], (int)tw[k][0]);
+                        v[k].y = __hiloint2double((int)tw[k][3], (int)tw[k][2]);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const double t0 = __dmul_rn(__dmul_rn(cf[k], v[2 * k].x), v[2 * k + 1].x);
+                    const double t1 = __dmul_rn(__dmul_rn(cf[k], v[2 * k].y), v[2 * k + 1].y);
+                    a0 = (g == 0 && k == 0) ? t0 : __dadd_rn(a0, t0);
+                    a1 = (g == 0 && k == 0) ? t1 : __dadd_rn(a1, t1);
+                }
+            }
+            if (r == reps - 1 && sp == 0) {
+                out[o * NPT5 + pt] = a0;
+                out[o * NPT5 + pt + 1] = a1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tb, 512);
+}
+
+template <int NW>
+int phaseb5_launch_t(const double *ops, const uint4 *table, double *out, int blocks, int reps, cudaStream_t st) {
+    const size_t smem = 128 + sizeof(uint4) * NOUT * 40 + sizeof(double) * NSM5 * NPT5;
+    cudaFuncSetAttribute(phaseb5_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    phaseb5_kernel<NW><<<blocks, NW * 32, smem, st>>>(ops, table, out, reps);
+    return (int)cudaGetLastError();
+}
+
 template <int SRC, int NW>
 int phaseb_launch_t(const double *ops, const Term *table, double *out, int blocks, int reps, cudaStream_t st) {
     const size_t smem = 128 + sizeof(Term) * NOUT * NTERM + (SRC > 0 ? sizeof(double) * NSM_OPS * NPTS : 0);
@@ -312,6 +409,13 @@ int phaseb_launch(int src, int nw, const double *ops, const void *table, double 
     if (src == S && nw == W) return phaseb2_launch_t<S, W>(ops, t, out, blocks, reps, s);
     P(3, 8) P(3, 16) P(3, 24) P(4, 8) P(4, 16) P(4, 24)
 #undef P
+    if (src == 5) {
+        const uint4 *t5 = (const uint4 *)table;
+        if (nw == 8) return phaseb5_launch_t<8>(ops, t5, out, blocks, reps, s);
+        if (nw == 12) return phaseb5_launch_t<12>(ops, t5, out, blocks, reps, s);
+        if (nw == 16) return phaseb5_launch_t<16>(ops, t5, out, blocks, reps, s);
+        if (nw == 24) return phaseb5_launch_t<24>(ops, t5, out, blocks, reps, s);
+    }
     return -1;
 }
 

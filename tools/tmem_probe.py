@@ -104,4 +104,35 @@ for src, t in ((0, tab), (1, tab), (2, tab_smem), (3, tab_tm), (4, tab_smem)):
         pt_terms = sms * reps * NOUT * NTERM * NPTS
         res[f"phaseb_src{src}_w{nw}"] = {"point_terms_per_clk_sm": pt_terms / s / sms / (mhz * 1e6), "ms": s * 1e3,
                                          "bits_ok": ok, "mhz": mhz}
+# SRC 5: 64 points, packed production table, TMEM (ops < 128) / shared (>= 128) by operand
+NPT5 = 64
+ops5 = rng.uniform(0.9, 1.1, (NOPS, NPT5))
+c5 = rng.standard_normal((NOUT, NTERM))
+p5 = rng.integers(0, NOPS, (NOUT, NTERM))
+q5 = rng.integers(0, NOPS, (NOUT, NTERM))
+packed = np.zeros((NOUT, 40, 16), dtype=np.uint8)
+for o in range(NOUT):
+    for g in range(8):
+        packed[o, 5 * g:5 * g + 4] = c5[o, 8 * g:8 * g + 8].astype("<f8").view(np.uint8).reshape(4, 16)
+        pq = (p5[o, 8 * g:8 * g + 8] | (q5[o, 8 * g:8 * g + 8] << 8)).astype("<u2")
+        packed[o, 5 * g + 4] = pq.view(np.uint8)
+want5 = np.empty((NOUT, NPT5))
+for o in range(NOUT):
+    acc = None
+    for k in range(NTERM):
+        t = (c5[o, k] * ops5[p5[o, k]]) * ops5[q5[o, k]]
+        acc = t if acc is None else acc + t
+    want5[o] = acc
+d_ops5 = torch.from_numpy(ops5).cuda()
+d_tab5 = torch.from_numpy(packed.reshape(-1).copy()).cuda()
+for nw in (8, 12, 16, 24):
+    d_out = torch.zeros((NOUT, NPT5), dtype=torch.float64, device="cuda")
+    reps = 64
+    rc = lib.phaseb_launch(5, nw, d_ops5.data_ptr(), d_tab5.data_ptr(), d_out.data_ptr(), sms, reps, st)
+    torch.cuda.synchronize()
+    ok = d_out.cpu().numpy().tobytes() == want5.tobytes()
+    s5, mhz = timed(lambda: lib.phaseb_launch(5, nw, d_ops5.data_ptr(), d_tab5.data_ptr(), d_out.data_ptr(), sms,
+                                              reps, st))
+    res[f"phaseb_src5_w{nw}"] = {"point_terms_per_clk_sm": sms * reps * NOUT * NTERM * NPT5 / s5 / sms / (mhz * 1e6),
+                                 "ms": s5 * 1e3, "bits_ok": ok, "mhz": mhz, "rc": rc}
 print(json.dumps(res, indent=1))
