@@ -52,6 +52,7 @@ class DeviceKernel:
 
     site_id = "kernel"
     space_kind = D4_SPACE
+    idempotent = True    # outputs are a pure function of the inputs (run_loop may replay a launch)
     extra_flags = 0   # SB_LAUNCH_* flags added to every launch (tools/sweep.py --flags)
     default_params: LaunchParams = LaunchParams(64, 8, 32)
 
@@ -370,6 +371,7 @@ class LevelRK4Stage(_LevelKernel):
 
     site_id = "rk4_level"
     space_kind = RK4_SPACE
+    idempotent = False   # stages 2-3 update the RK accumulators in place
     default_params = LaunchParams(64, 4, 16, 1)
     NAMES = ("phi_s", "pi_s", "phi0", "pi0", "acc_phi", "acc_pi", "phi_out", "pi_out")
 
