@@ -240,3 +240,36 @@ def test_boxes_with_empty_spaces_are_skipped(monkeypatch):
         if all(h > l for l, h in zip(lo, hi)):
             oracle.lap4(want, u, G, (lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]), k.k2)
         assert d.download().tobytes() == want.tobytes(), b
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_multi_box_levels_random_shapes(seed):
+    """Random levels (9-40 boxes) x random launch shapes (tile 32/64/128,
+    tile rows, z chunk, scalar or paired points) for the ten-output set and
+    the Laplacian: every box bit-exact (inline table for <= 8 boxes, device
+    table above)."""
+    from paper_1308_1343_b200.kernels import LevelFourthOrderAll, LevelLaplacian4
+    rng = np.random.default_rng(100 + seed)
+    nbox = int(rng.integers(9, 41))
+    boxes = random_level(nbox, 200 + seed, region=(int(rng.integers(40, 90)), int(rng.integers(20, 50)),
+                                                   int(rng.integers(10, 40))), origin=tuple(int(v) for v in
+                                                                                           rng.integers(-30, 30, 3)))
+    srcs, host = grids(boxes, 300 + seed)
+    k = inputs.D4Constants.for_spacing(float(rng.uniform(0.01, 0.1)))
+    tx = int(rng.choice([32, 64, 128]))
+    np_ = int(rng.choice([1, 2]))
+    ty = int(rng.choice([1, 2, 4])) if (tx // np_) * 4 <= 256 else 1
+    while (tx // np_) * ty % 32:
+        ty *= 2
+    p = LaunchParams(tx, ty, int(rng.integers(1, 40)), np_)
+    outs = [[DeviceGrid(b.extents, 0, lower=b.lo) for _ in range(10)] for b in boxes]
+    LevelFourthOrderAll(outs, srcs, k).launch(None, p)
+    dsts = [DeviceGrid(b.extents, 0, lower=b.lo) for b in boxes]
+    LevelLaplacian4(dsts, srcs, k).launch(None, p)
+    for b, u, os_, d in zip(boxes, host, outs, dsts):
+        nx, ny, nz = b.extents
+        want = [np.empty((nz, ny, nx)) for _ in range(10)]
+        oracle.d4_all(want, u, G, (0, nx, 0, ny, 0, nz), k)
+        for i in range(10):
+            assert os_[i].download().tobytes() == want[i].tobytes(), (p, b, i)
+        assert d.download().tobytes() == want[9].tobytes(), (p, b)
