@@ -82,6 +82,27 @@ def fp64_peak() -> float | None:
         return None
 
 
+def ncu_kernel(name_part: str) -> dict | None:
+    """This round's committed ncu summary of a kernel (profiles/r02/ncu_kernels.json)."""
+    p = ROOT / "profiles" / "r02" / "ncu_kernels.json"
+    try:
+        for e in json.loads(p.read_text()):
+            if name_part in e.get("kernel", ""):
+                return e
+    except (OSError, ValueError):
+        pass
+    return None
+
+
+def lds_peak() -> float | None:
+    """Measured shared-memory wavefronts/s of this B200 pool (tools/pipe_ceiling.py)."""
+    p = ROOT / "profiles" / "r01" / "pipe_ceiling.json"
+    try:
+        return float(json.loads(p.read_text())["smem_wavefronts_per_s"])
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def ncu_traffic() -> float | None:
     """dram bytes (read+write) per d4_all launch from the committed ncu summary."""
     p = ROOT / "profiles" / "ncu_summary.json"
@@ -413,6 +434,16 @@ def extra_legs(args, dev: int, stream, hbm_peak: float) -> dict:
                      "algorithmic_bytes_per_step": p.canonical_bytes},
         "gpu_launches": K, "clocks": clk,
         "input_sha256": inputs.sha256(np.stack(p.host_u)), "poly_sha256": inputs.sha256(p.poly.coef)}
+    # the binding resource: shared-memory wavefronts (count per sweep from the
+    # committed ncu capture, rate from this run's time)
+    e, lp = ncu_kernel("rhs24_kernel"), lds_peak()
+    if e and lp and e.get("shared_wavefronts"):
+        wf = e["shared_wavefronts"] / (step_ms * 1e-3)
+        out["c5_rhs24_192^3"]["binding"] = {
+            "resource": "shared-memory wavefronts", "per_sweep": e["shared_wavefronts"],
+            "per_point": e["shared_wavefronts"] / p.updates, "achieved_per_s": wf, "peak_per_s": lp,
+            "frac": wf / lp, "source": "wavefront count: ncu --set full, profiles/r02/ncu_kernels.json (not this run); "
+                                      "peak: profiles/r01/pipe_ceiling.json"}
     del p
     torch.cuda.empty_cache()
     return out
