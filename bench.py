@@ -399,6 +399,13 @@ def extra_legs(args, dev: int, stream, hbm_peak: float) -> dict:
                      "survey_34pass_gbs": p.survey_canonical_bytes / (step_ms * 1e-3) / 1e9},
         "gpu_launches": 2 * K, "clocks": clk,
         "input_sha256": {"phi0": inputs.sha256(p.host_phi), "pi0": inputs.sha256(p.host_pi)}}
+    la, lb = ncu_kernel("rkpair_kernel<2"), ncu_kernel("rkpair_kernel<3")
+    if la and lb:
+        out["c3_wave_rk4_384^3"]["binding"] = {
+            "resource": "instruction issue / FP64 pipe (temporal blocking moved it off HBM)",
+            "pair_LA": {k: la.get(k) for k in ("duration_us", "issue_active_pct", "fp64_pipe_pct", "dram_pct_of_peak")},
+            "pair_LB": {k: lb.get(k) for k in ("duration_us", "issue_active_pct", "fp64_pipe_pct", "dram_pct_of_peak")},
+            "source": "ncu --set full, profiles/r02/ncu_kernels.json (not this run)"}
     del p
     torch.cuda.empty_cache()
 
