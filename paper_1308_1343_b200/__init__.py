@@ -10,7 +10,8 @@ from .traverse import (  # noqa: F401
     index_space_to_bbox, run_loop, run_static,
 )
 from .tuner import (  # noqa: F401
-    ExecParams, LaunchParams, LaunchSpace, LoopSetup, PlanSpace, TopologyConfig, Tuner, TuningCache,
+    ExecParams, LaunchParams, LaunchSpace, LoopSetup, PlanSpace, TopologyConfig, Tuner, TuningCache, device_setup,
 )
+from .level import Box, Lattice, boxes_of, compact_level  # noqa: F401
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"
