@@ -227,6 +227,11 @@ SB_API int sb_d2_all_boxes(const sb_d4_all_job *jobs, int32_t njobs, sb_d4_const
 /* Free the library's cached device box tables (waits for the device). */
 SB_API int sb_release_tables(void);
 
+/* Release every device allocation the library owns (box tables, the
+ * barrier-counter pools of sb_init); waits for the devices.  The library
+ * stays usable: later calls allocate again on first use. */
+SB_API int sb_shutdown(void);
+
 /* K4 — periodic refill of the ghost shell of `a` (every ghost point becomes
  * the interior point at its periodic image). */
 SB_API int sb_ghost_periodic(sb_array a, void *stream);

@@ -30,6 +30,7 @@ EXPORTS = (
     "sb_rhs24", "sb_copy_regions", "sb_copy_h2d", "sb_copy_d2h", "sb_copy_h2d_planes", "sb_copy_d2h_planes",
     "sb_copy_h2d_planes_staged", "sb_rk4_stage_zslab", "sb_rk4_pair", "sb_rk4_pair_zslab", "sb_lap7_iterate",
     "sb_d4_all_boxes", "sb_d2_all_boxes", "sb_rk4_stage_boxes", "sb_release_tables", "sb_enable_peer_access",
+    "sb_shutdown",
 )
 SB_MAX_COPY_JOBS = 64
 
@@ -111,6 +112,7 @@ def _declare(lib) -> None:
         "sb_d2_all_boxes": ([C.POINTER(sb_d4_all_job), i32, sb_d4_constants, sb_launch, vp], C.c_int),
         "sb_rk4_stage_boxes": ([i32, C.POINTER(sb_rk4_box_job), i32, sb_rk4_constants, sb_launch, vp], C.c_int),
         "sb_release_tables": ([], C.c_int),
+        "sb_shutdown": ([], C.c_int),
         "sb_enable_peer_access": ([C.c_int], C.c_int),
         "sb_ghost_periodic": ([sb_array, vp], C.c_int),
         "sb_rk4_stage": ([i32, C.POINTER(sb_rk4_fields), sb_space, sb_rk4_constants, sb_launch, vp], C.c_int),
@@ -176,6 +178,13 @@ def call(name: str, *args) -> None:
 
 
 _inited: set[int] = set()
+
+
+def shutdown() -> None:
+    """sb_shutdown: free the library-owned device memory (box tables, barrier
+    counters); the next use on a device re-initialises it."""
+    call("sb_shutdown")
+    _inited.clear()
 
 
 def init_current_device() -> None:

@@ -352,6 +352,12 @@ int sb_rk4_stage_boxes(int32_t stage, const sb_rk4_box_job *jobs, int32_t njobs,
 
 int sb_release_tables(void) { return release_box_tables(); }
 
+int sb_shutdown(void) {
+    int rc = release_box_tables();
+    int rc2 = release_barrier_counters();
+    return rc ? rc : rc2;
+}
+
 int sb_ghost_periodic(sb_array a, void *stream) {
     int rc = check_array(a, 0, "ghost_periodic");
     if (rc) return rc;

@@ -56,6 +56,7 @@ int launch_lap7_iterate(const sb_array &a, const sb_array &b, const sb_space &sp
 // sb_lap7_iterate's grid-barrier counters (lap7.cu): reserve the device's
 // pool (sb_init), and the slot of a (device, stream) pair.
 int reserve_barrier_counters(int dev);
+int release_barrier_counters();
 int barrier_counter(int dev, cudaStream_t st, unsigned long long **out);
 int launch_diff1d(int kind, double *dst, const double *src, int n, cudaStream_t st);
 

@@ -195,6 +195,21 @@ int reserve_locked(int dev) {
 }
 }  // namespace
 
+int release_barrier_counters() {
+    std::lock_guard<std::mutex> lock(g_ctr_mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto &kv : g_ctr_pool) {
+        cudaSetDevice(kv.first);
+        cudaFree(kv.second);   // implicitly waits for the device's work
+    }
+    cudaSetDevice(cur);
+    g_ctr_pool.clear();
+    g_ctr.clear();
+    g_ctr_used.clear();
+    return SB_OK;
+}
+
 int reserve_barrier_counters(int dev) {
     std::lock_guard<std::mutex> lock(g_ctr_mu);
     return reserve_locked(dev);

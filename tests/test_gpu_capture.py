@@ -94,3 +94,38 @@ def test_lap7_iterate_captured_on_first_use():
         x, y = y, x
     want = x[1:-1, 1:-1, 1:-1]
     assert res.download().tobytes() == np.ascontiguousarray(want).tobytes()
+
+
+def test_shutdown_releases_and_library_stays_usable():
+    """sb_shutdown frees the box tables and barrier counters; the next calls
+    allocate again (lap7_iterate, a >8-box level)."""
+    import torch
+    from paper_1308_1343_b200 import inputs
+    from paper_1308_1343_b200.grid import DeviceGrid
+    from paper_1308_1343_b200.kernels import Laplacian7, LevelLaplacian4
+    from paper_1308_1343_b200.level import Box
+    from paper_1308_1343_b200.traverse import IndexSpace
+    from paper_1308_1343_b200.tuner import LaunchParams
+    boxes = [Box((6 * i, 0, 0), (6 * i + 4, 5, 6)) for i in range(10)]
+    srcs = [DeviceGrid(b.extents, 2, lower=b.lo) for b in boxes]
+    dsts = [DeviceGrid(b.extents, 0, lower=b.lo) for b in boxes]
+    lvl = LevelLaplacian4(dsts, srcs, inputs.D4Constants.for_spacing(0.1))
+    lvl.launch(None, LaunchParams(32, 4, 4, 2))
+    n = 12
+    u = inputs.c1_field(n, 3)
+    c0, c1 = inputs.c1_constants(n)
+    a, b = DeviceGrid((n,) * 3, 1), DeviceGrid((n,) * 3, 1)
+    a.upload(u, with_ghosts=True)
+    b.upload(u, with_ghosts=True)
+    k = Laplacian7(b, a, c0, c1)
+    k.iterate(a, b, IndexSpace((0, 0, 0), (n, n, n)), 3)
+    torch.cuda.synchronize()
+    _lib.shutdown()
+    for s in srcs:
+        s.fill_(1.0)
+    lvl.launch(None, LaunchParams(32, 4, 4, 2))
+    res = k.iterate(a, b, IndexSpace((0, 0, 0), (n, n, n)), 3)
+    torch.cuda.synchronize()
+    # a constant field: the 4th-order Laplacian is exactly zero everywhere
+    assert all(float(d.interior().abs().max()) == 0.0 for d in dsts)
+    assert res.download().shape == (n, n, n)
