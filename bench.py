@@ -648,12 +648,20 @@ def run_ours(args) -> None:
     peaks = measured_peaks()
     peak = float(peaks.get("hbm_gbs", 6650.0))
     extra = zslab = None
+    # the extra legs never cost the headline line: a failure is recorded, not raised
     if not args.no_extra and world == 1:
         del prob.outs, prob.kernel, prob.src
         torch.cuda.empty_cache()
-        extra = extra_legs(args, dev, stream, peak)
+        try:
+            extra = extra_legs(args, dev, stream, peak)
+        except Exception as e:  # noqa: BLE001
+            extra = {"error": repr(e)[:400]}
+            torch.cuda.synchronize()
     if not args.no_extra and world > 1:
-        zslab = zslab_legs(args, dist, rank, world, backend, dev)
+        try:
+            zslab = zslab_legs(args, dist, rank, world, backend, dev)
+        except Exception as e:  # noqa: BLE001
+            zslab = {"error": repr(e)[:400]}
 
     if rank != 0:
         if dist:
@@ -671,7 +679,10 @@ def run_ours(args) -> None:
                     "sample": cpu["sample"] + f", {c2.threads} threads, piece kernel = oracle numpy expression trees"})
         one = c2.sample(args.ref_seconds_1t, 1, 4)
         cpu["one_thread"] = dict(one, kind="port", engine=c2.engine_name)
-        cpu["c1_reference_drivers"] = c1_reference_drivers()
+        try:
+            cpu["c1_reference_drivers"] = c1_reference_drivers()
+        except Exception as e:  # noqa: BLE001
+            cpu["c1_reference_drivers"] = {"error": repr(e)[:300]}
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
