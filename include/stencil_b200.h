@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define SB_ABI_VERSION 1
+#define SB_ABI_VERSION 2   /* 2: level box tables, multi-box d4_all/d2_all/RK stages, peer access, shutdown */
 
 #if defined(__GNUC__)
 #define SB_API __attribute__((visibility("default")))

@@ -18,6 +18,7 @@ from .errors import DeviceError, ResourceError, UsageError
 LIB_PATH = Path(__file__).resolve().parent / "libstencil_b200.so"
 
 SB_OK, SB_USAGE, SB_RESOURCE, SB_CUDA = 0, 1, 2, 3
+SB_ABI_VERSION = 2   # include/stencil_b200.h
 SB_MAX_BOXES = 8
 SB_N_D4_OUT = 10
 SB_N_VARS = 24
@@ -160,6 +161,9 @@ def load(path: str | os.PathLike | None = None):
                 raise DeviceError(f"{p} not built; run __graft_entry__.build() (no CPU fallback exists)")
             lib = C.CDLL(str(p))
             _declare(lib)
+            if lib.sb_abi_version() != SB_ABI_VERSION:
+                raise DeviceError(f"{p} has ABI version {lib.sb_abi_version()}, this package needs "
+                                  f"{SB_ABI_VERSION}: rebuild it (__graft_entry__.build())")
             _lib = lib
         return _lib
 

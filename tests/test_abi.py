@@ -27,7 +27,7 @@ def test_header_and_binding_agree():
 def test_library_exports_every_declared_symbol(lib):
     for name in _lib.EXPORTS:
         assert hasattr(lib, name), name
-    assert lib.sb_abi_version() == 1
+    assert lib.sb_abi_version() == _lib.SB_ABI_VERSION == 2
 
 
 def test_struct_layouts_match_header():
