@@ -100,6 +100,47 @@ __global__ void ldtm_bw_kernel(unsigned long long *out, int iters) {
     if (acc == 0x12345678u) out[blockIdx.x] = acc;
 }
 
+// ---- does LDTM share the shared-memory data path? -------------------------
+// 8 LDS.64 (optional) + K tcgen05.ld.32x32b.x2 per step, integer accumulation
+template <int K>
+__global__ void ldtm_lds_mix_kernel(unsigned long long *out, int iters, int with_lds) {
+    __shared__ uint32_t slot;
+    __shared__ double buf[4096];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) buf[i] = i;
+    if (warp == 0) tmem_alloc(&slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t base = slot + ((uint32_t)(32 * (warp & 3)) << 16);
+    unsigned long long s = 0;
+    uint32_t acc = 0;
+    int b = (warp * 32) % 2048;
+    for (int it = 0; it < iters; ++it) {
+        if (with_lds) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s ^= __double_as_longlong(buf[((b + k * 256) & 2047) + lane]);
+            b += 32;
+        }
+        if constexpr (K > 0) {
+            uint32_t v[K][2];
+#pragma unroll
+            for (int k = 0; k < K; ++k) ld_x2(base + ((it * 2 + k * 24) & 255), v[k][0], v[k][1]);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                pin(v[k][0]);
+                pin(v[k][1]);
+                acc ^= v[k][0] ^ v[k][1];
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(slot, 512);
+    if ((s ^ acc) == 0x12345678u) out[blockIdx.x] = s ^ acc;
+}
+
 // ---- phase-B loop ------------------------------------------------------------
 constexpr int NOPS = 240, NOUT = 24, NTERM = 64, NPTS = 128, NSM_OPS = 112;
 
@@ -417,6 +458,15 @@ int phaseb_launch(int src, int nw, const double *ops, const void *table, double 
         if (nw == 24) return phaseb5_launch_t<24>(ops, t5, out, blocks, reps, s);
     }
     return -1;
+}
+
+int mix_launch(int k, int with_lds, unsigned long long *out, int blocks, int threads, int iters, void *st) {
+    cudaStream_t s = (cudaStream_t)st;
+    if (k == 0) ldtm_lds_mix_kernel<0><<<blocks, threads, 0, s>>>(out, iters, with_lds);
+    else if (k == 4) ldtm_lds_mix_kernel<4><<<blocks, threads, 0, s>>>(out, iters, with_lds);
+    else if (k == 8) ldtm_lds_mix_kernel<8><<<blocks, threads, 0, s>>>(out, iters, with_lds);
+    else return -1;
+    return (int)cudaGetLastError();
 }
 
 int last_error() { return (int)cudaDeviceSynchronize(); }

@@ -61,6 +61,16 @@ for n, k in ((2, 4), (2, 8), (2, 16), (4, 4), (4, 8), (8, 4), (8, 8)):
         res[f"ldtm_x{n}_k{k}_w{warps}_B_per_clk_sm"] = by / s / sms / (mhz * 1e6)
         res[f"ldtm_x{n}_k{k}_w{warps}_instr_per_clk_sm"] = sms * warps * iters * k / s / sms / (mhz * 1e6)
 
+# LDTM.x2 vs LDS.64: separate or shared data path?  (8 LDS.64 and/or K LDTM per step)
+lib.mix_launch.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
+for k, wl in ((0, 1), (8, 0), (8, 1), (4, 1)):
+    for warps in (8, 16):
+        iters = 4096
+        s, mhz = timed(lambda: lib.mix_launch(k, wl, out.data_ptr(), sms, warps * 32, iters, st))
+        per = sms * warps * iters / s / sms / (mhz * 1e6)
+        res[f"mix_lds{8 * wl}_ldtm{k}_w{warps}"] = {"ms": s * 1e3, "lds_wavefronts_per_clk_sm": per * 8 * wl * 2,
+                                                     "ldtm_instr_per_clk_sm": per * k}
+
 # phase B
 NOPS, NOUT, NTERM, NPTS, NSM = 240, 24, 64, 128, 112
 rng = np.random.default_rng(7)
