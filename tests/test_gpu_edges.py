@@ -193,3 +193,52 @@ def test_d4_all_nonfinite_inputs_follow_ieee():
         assert np.array_equal(nan_w, nan_g), i
         assert np.array_equal(got[~nan_g].view(np.uint64), want[i][~nan_w].view(np.uint64)), i
         assert np.isinf(want[i]).any() == np.isinf(got).any(), i
+
+
+@pytest.mark.parametrize("g", [3, 4, 7])
+def test_wider_ghost_zones(g):
+    """Ghost widths beyond the stencil radius (the TMA maps start at the
+    first ghost row, interior at (xpad, g, g)): the ten outputs and the
+    level Laplacian read the right points."""
+    from paper_1308_1343_b200.grid import DeviceGrid
+    from paper_1308_1343_b200.kernels import LevelLaplacian4
+    from paper_1308_1343_b200.level import Box
+    ext = (29, 14, 10)
+    u, k, src, outs, kern = d4_setup(ext, g=g, seed=50 + g)
+    kern.launch(kern.full_space(), LaunchParams(64, 2, 4, 2))
+    want = [np.empty(ext[::-1]) for _ in range(10)]
+    oracle.d4_all(want, u, g, (0, ext[0], 0, ext[1], 0, ext[2]), k)
+    for i in range(10):
+        assert same(outs[i].download(), want[i]), (g, i)
+    boxes = [Box((0, 0, 0), (28, 13, 9)), Box((40, 0, 0), (52, 6, 4))]
+    rng = np.random.default_rng(g)
+    srcs, hosts, dsts = [], [], []
+    for b in boxes:
+        nx, ny, nz = b.extents
+        a = rng.uniform(-1, 1, (nz + 2 * g, ny + 2 * g, nx + 2 * g))
+        d = DeviceGrid(b.extents, g, lower=b.lo)
+        d.upload(a, with_ghosts=True)
+        srcs.append(d)
+        hosts.append(a)
+        dsts.append(DeviceGrid(b.extents, 0, lower=b.lo))
+    LevelLaplacian4(dsts, srcs, k).launch(None, LaunchParams(32, 4, 3, 2))
+    for b, a, d in zip(boxes, hosts, dsts):
+        nx, ny, nz = b.extents
+        w = np.empty((nz, ny, nx))
+        oracle.lap4(w, a, g, (0, nx, 0, ny, 0, nz), k.k2)
+        assert same(d.download(), w), (g, b)
+
+
+@pytest.mark.parametrize("schedule", ["lap_pairs", "stages"])
+def test_rk4_periodic_ghost_width_three(schedule):
+    """A periodic box with ghost width 3: the fused refresh writes all three
+    ghost layers (images at distance up to 3) and the step still equals the
+    oracle's (which fills the whole 3-wide shell)."""
+    from paper_1308_1343_b200.configs import C3WaveRK4
+    n, g = 14, 3
+    p = C3WaveRK4(n=n, seed=21, g=g, schedule=schedule).setup()
+    p.run(LaunchParams(32, 4, 5, 1))
+    wphi, wpi = oracle.rk4_step(p.host_phi, p.host_pi, g, p.c)
+    assert same(p.phi_with_ghosts(), wphi)
+    I = (slice(g, g + n),) * 3
+    assert same(p.outputs()[1], wpi[I])
