@@ -92,7 +92,10 @@ def cmd_config_bench(args) -> int:
     kern = getattr(prob, "kernel", None) or prob.rk
     space = kern.launch_space()
     ext = kern.full_space().extents if hasattr(kern, "full_space") else (prob.n,) * 3
-    setup = LoopSetup(f"config{args.config}", ext)
+    # device tuning key (tuner.device_setup): site, extents, grid pitch, SM count
+    pitch = kern.pitch_class() if hasattr(kern, "pitch_class") else prob.rk.phi0.sy
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    setup = LoopSetup(f"config{args.config}", ext, pitch=pitch, sm_count=sms)
     tuner = Tuner(_topology(args))
     default = getattr(kern, "default_params", None) or getattr(kern, "params")
     tuner.prime(setup, space, default)
