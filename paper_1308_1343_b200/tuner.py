@@ -429,6 +429,9 @@ class LaunchSpace:
             raise UsageError(f"tile_x {p.tile_x} not in {self.tile_xs}")
         if p.tile_y < 1 or p.z_chunk < 1:
             raise UsageError("tile_y and z_chunk must be positive")
+        if p.tile_y not in self.tile_ys:
+            # e.g. rhs24's CTA shape is fixed: other tile heights would be the same kernel
+            raise UsageError(f"tile_y {p.tile_y} not in {self.tile_ys}")
         if p.points_per_thread not in self.points:
             raise UsageError(f"points_per_thread {p.points_per_thread} not in {self.points}")
         cap = self.max_threads_pair if p.points_per_thread == 2 else self.max_threads_scalar
