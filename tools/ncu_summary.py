@@ -26,6 +26,8 @@ METRICS = {
     "block": ("launch__block_size", 1),
     "smem_per_block": ("launch__shared_mem_per_block", 1),
     "sm_clock_mhz": ("smsp__cycles_elapsed.avg.per_second", 1),
+    "l2_to_sm_read_bytes": ("l1tex__m_xbar2l1tex_read_bytes.sum", 1),
+    "l2_to_sm_tma_read_bytes": ("l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum", 1),
 }
 # unit -> factor to the summary's unit (us, bytes, MHz)
 UNITS = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6,
