@@ -37,6 +37,7 @@ the same kernel.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -474,12 +475,27 @@ def zslab_legs(args, dist, rank: int, world: int, backend: str, dev: int) -> dic
     if backend == "nccl" and args.zslab_staged:   # opt-in: NCCL point-to-point exchange baseline
         modes.append(("staged", "device"))
     res = {"box": [n, n, n], "slabs": world, "schedule": "lap_pairs", "scaling": "strong (one box over N GPUs)"}
+    flag_dev = "cuda" if backend == "nccl" else "cpu"
+
+    def agree(ok: bool) -> bool:
+        """All ranks learn whether every rank got this far (a rank that failed
+        locally still joins, so no rank is left waiting in a collective)."""
+        f = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64, device=flag_dev)
+        dist.all_reduce(f, op=dist.ReduceOp.MIN)
+        return f.item() == 1.0
+
     for transport, sync in modes:
         me = None
         try:
-            me = ZSlabRank(n, rank, world, g, c, dist, schedule="lap_pairs", transport=transport, sync=sync)
-            me.slab.upload(host_phi, host_pi)
-            torch.cuda.synchronize()
+            err = None
+            try:    # setup failures (IPC mapping, peer access) are agreed on before any step
+                me = ZSlabRank(n, rank, world, g, c, dist, schedule="lap_pairs", transport=transport, sync=sync)
+                me.slab.upload(host_phi, host_pi)
+                torch.cuda.synchronize()
+            except Exception as e:  # noqa: BLE001
+                err = e
+            if not agree(err is None):
+                raise RuntimeError(f"z-slab setup failed on some rank (this rank: {err!r})")
             dist.barrier()
             me.step()
             torch.cuda.synchronize()
@@ -519,9 +535,9 @@ def run_ours(args) -> None:
     if world > 1:
         import torch.distributed as dist
         if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev), timeout=datetime.timedelta(seconds=900))
         else:
-            dist.init_process_group(backend)
+            dist.init_process_group(backend, timeout=datetime.timedelta(seconds=900))
 
     from paper_1308_1343_b200 import _build, inputs
     from paper_1308_1343_b200.configs import C2FourthOrder
