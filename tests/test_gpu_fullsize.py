@@ -39,10 +39,12 @@ def _threads() -> int:
 
 # -- config 2: all ten outputs of the whole 256^3 box ---------------------------
 
-def test_c2_whole_volume_all_ten_outputs():
+@pytest.mark.parametrize("shape", [None, (32, 4, 4, 2)])   # default launch / the bench's tuned shape
+def test_c2_whole_volume_all_ten_outputs(shape):
     from paper_1308_1343_b200.configs import C2FourthOrder
+    from paper_1308_1343_b200.tuner import LaunchParams
     p = C2FourthOrder().setup()
-    p.run()
+    p.run(None if shape is None else LaunchParams(*shape))
     n, g = p.n, p.g
     want = [np.empty((n, n, n)) for _ in range(10)]
     oracle.run_static(lambda z0, z1: oracle.d4_all(want, p.host_u, g, (0, n, 0, n, z0, z1), p.k), 0, n, _threads())
