@@ -62,6 +62,13 @@ class DeviceKernel:
     def __call__(self, piece: IndexSpace) -> None:
         self.launch(piece, self.default_params)
 
+    def launch_plan(self, plan, params: LaunchParams | None = None, stream=None) -> None:
+        """The fast path for a reference plan (``build_plan``, traverse.py:130-156):
+        its pieces partition ``plan.space``, so executing all of them is ONE
+        launch over that space (tiles = CTAs) — the result ``execute_plan``
+        would produce piece by piece, bit for bit."""
+        self.launch(plan.space, params or self.default_params, stream=stream)
+
     def launch(self, space: IndexSpace, params: LaunchParams, stream=None) -> None:
         raise NotImplementedError
 

@@ -457,3 +457,32 @@ def test_d2_all_golden_and_oracle(golden):
                 assert bits_equal(got, want[i]), (n, params, i, first_diff(got, want[i]))
                 if n == m["n"]:
                     assert bits_equal(got, a["c2o2_out"][i])
+
+
+def test_launch_plan_equals_execute_plan_piece_by_piece():
+    """kernel.launch_plan(build_plan(...)) — one launch over the plan's space —
+    writes exactly what execute_plan writes piece by piece (traverse.py:130-209)."""
+    from paper_1308_1343_b200.grid import DeviceGrid
+    from paper_1308_1343_b200.kernels import FourthOrderAll
+    from paper_1308_1343_b200.traverse import IndexSpace, build_plan, execute_plan
+    from paper_1308_1343_b200.tuner import ExecParams
+    rng = np.random.default_rng(41)
+    ext, g = (45, 19, 13), 2
+    u = rng.uniform(-1, 1, (ext[2] + 2 * g, ext[1] + 2 * g, ext[0] + 2 * g))
+    k = inputs.D4Constants.for_spacing(1.0 / 45)
+    src = DeviceGrid(ext, g, lower=(3, -2, 5))
+    src.upload(u)
+    space = IndexSpace((4, -1, 6), (44, 15, 17))
+    plan = build_plan(space, ExecParams((2, 1, 2), (16, 8, 4), (2, 1, 1), 4))
+    outs = []
+    for run in ("pieces", "plan"):
+        o = [DeviceGrid(ext, 0, lower=(3, -2, 5)).fill_(0.5) for _ in range(10)]
+        kern = FourthOrderAll(o, src, k)
+        if run == "pieces":
+            execute_plan(plan, kern, 2, 2)
+        else:
+            kern.launch_plan(plan)
+        outs.append([x.download() for x in o])
+    for a, b in zip(*outs):
+        assert a.tobytes() == b.tobytes()
+    assert not np.all(outs[1][9] == 0.5)
