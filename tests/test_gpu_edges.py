@@ -242,3 +242,56 @@ def test_rk4_periodic_ghost_width_three(schedule):
     assert same(p.phi_with_ghosts(), wphi)
     I = (slice(g, g + n),) * 3
     assert same(p.outputs()[1], wpi[I])
+
+
+def _adversarial_poly(seed: int) -> "inputs.PolyTable":
+    """Term tables a fixed seed never draws: operand indices at both ends of
+    0..239, p == q, one operand reused by every term of an output, signed
+    zeros, and coefficients large enough to overflow to +-inf or small
+    enough to land in the subnormals."""
+    rng = np.random.default_rng(seed)
+    n_out, n_t = inputs.N_VARS, inputs.N_TERMS
+    coef = rng.standard_normal((n_out, n_t))
+    p = rng.integers(0, 240, (n_out, n_t)).astype(np.int32)
+    q = rng.integers(0, 240, (n_out, n_t)).astype(np.int32)
+    p[0, :], q[0, :] = 0, 239                  # the first and last operand rows
+    p[1, :] = q[1, :] = 7                      # v_7 * v_7, 64 times
+    coef[2, ::2], coef[2, 1::2] = 0.0, -0.0    # signed zeros
+    coef[3, :] = 1e307                         # positive u*u products: the sum overflows to +inf (no inf - inf)
+    p[3, :] = q[3, :] = 10 * (np.arange(n_t) % 24)
+    coef[4, :] = 1e-310                        # subnormal products
+    p[5, :] = np.arange(n_t) % 240
+    q[5, :] = 239 - p[5, :]
+    coef[6, 10] = np.inf                       # one infinite coefficient
+    return inputs.PolyTable(coef, p, q)
+
+
+@pytest.mark.parametrize("ext,lo,hi", [((13, 7, 5), (0, 0, 0), (13, 7, 5)), ((21, 9, 6), (3, 1, 2), (20, 8, 5))])
+def test_rhs24_adversarial_tables_and_subspaces(ext, lo, hi):
+    """The config-5 kernel takes any term table: edge operand indices,
+    repeated operands, signed zeros, overflow and subnormal products all
+    follow the oracle's IEEE evaluation bit for bit, on a ragged box and on a
+    sub-space (the outputs outside it keep their sentinel)."""
+    from paper_1308_1343_b200.grid import DeviceGrid
+    from paper_1308_1343_b200.kernels import Rhs24
+    from paper_1308_1343_b200.traverse import IndexSpace
+    g = 2
+    nx, ny, nz = ext
+    rng = np.random.default_rng(sum(ext))
+    host = [rng.uniform(0.9, 1.1, (nz + 2 * g, ny + 2 * g, nx + 2 * g)) for _ in range(inputs.N_VARS)]
+    ins = []
+    for u in host:
+        d = DeviceGrid(ext, g)
+        d.upload(u, with_ghosts=True)
+        ins.append(d)
+    outs = [DeviceGrid(ext, 0).fill_(-3.25) for _ in range(inputs.N_VARS)]
+    poly = _adversarial_poly(sum(ext))
+    k = inputs.D4Constants.for_spacing(1.0 / 19)
+    with np.errstate(all="ignore"):
+        Rhs24(ins, outs, k, poly).launch(IndexSpace(lo, hi), LaunchParams(32, 4, 3, 2))
+        want = [np.full((nz, ny, nx), -3.25) for _ in range(inputs.N_VARS)]
+        oracle.rhs24(want, host, g, (lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]), k, poly)
+    got = [o.download() for o in outs]
+    assert np.isinf(want[3][lo[2], lo[1], lo[0]]) and want[2][lo[2], lo[1], lo[0]] == 0.0
+    for o in range(inputs.N_VARS):
+        assert same(got[o], want[o]), o
